@@ -1,0 +1,1347 @@
+// api.cu -- the C ABI of libgss_b200.so (include/gss_b200.h): context, batch
+// orchestration of scheduler::enhance_batch (scheduler.hpp:314-365) over many
+// independent SuperSegments, and the stage entry points. Host code only; every
+// numerical step is a kernel launch on the context's stream. There is no CPU
+// implementation of any stage in this library.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/gss_b200.h"
+#include "kernels.h"
+
+namespace gssb {
+
+namespace {
+thread_local std::string t_err;
+thread_local long long t_err_freq = -1;
+}  // namespace
+
+void set_thread_error(int code, const std::string& msg, long long freq) {
+  (void)code;
+  t_err = msg;
+  t_err_freq = freq;
+}
+
+struct Tables {
+  float2* tw = nullptr;
+  float* win = nullptr;
+};
+
+struct Fail {
+  gss_status code;
+  std::string msg;
+  long long freq;
+};
+
+}  // namespace gssb
+
+using namespace gssb;
+
+struct gss_b200_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  long long err_freq = -1;
+  long long launches = 0;
+  long long device_bytes = 0;
+  std::map<std::pair<int, int>, Tables> tables;
+  double stage_ms[GSS_B200_NUM_STAGES] = {0, 0, 0, 0, 0, 0, 0};
+  int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
+  int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
+};
+
+namespace {
+
+gss_status fail(gss_b200_ctx* c, gss_status code, const std::string& msg, long long freq = -1) {
+  if (c) {
+    c->err = msg;
+    c->err_freq = freq;
+  }
+  set_thread_error(code, msg, freq);
+  return code;
+}
+
+#define CU_TRY(ctx, expr)                                                                          \
+  do {                                                                                             \
+    cudaError_t e__ = (expr);                                                                      \
+    if (e__ != cudaSuccess)                                                                        \
+      return fail(ctx, GSS_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e__));      \
+  } while (0)
+
+const char* status_name(int code) {
+  switch (code) {
+    case GSS_SHAPE_ERROR: return "ShapeError";
+    case GSS_CONFIG_ERROR: return "ConfigError";
+    case GSS_SINGULAR_MATRIX_ERROR: return "SingularMatrixError";
+    case GSS_INPUT_TOO_SHORT_ERROR: return "InputTooShortError";
+    case GSS_EMPTY_TARGET_ERROR: return "EmptyTargetError";
+    case GSS_DEGENERATE_STATS_ERROR: return "DegenerateStatsError";
+    default: return "Error";
+  }
+}
+
+// ---- configuration validation (stft.hpp:25-35, wpe.hpp:22-29, scheduler.hpp:46-57)
+bool validate_stft(const gss_stft_config& s, std::string& why) {
+  if (s.fft_size <= 0 || s.shift <= 0) return why = "stft: fft_size and shift must be positive", false;
+  if (s.fft_size % s.shift != 0) return why = "stft: shift must divide fft_size for overlap-add", false;
+  if (s.sample_rate <= 0) return why = "stft: sample_rate must be positive", false;
+  return true;
+}
+bool validate_wpe(const gss_wpe_config& w, std::string& why) {
+  if (w.taps < 1 || w.delay < 1 || w.iterations < 1)
+    return why = "wpe: taps, delay and iterations must be >= 1", false;
+  if (w.psd_context < 0 || w.regularization < 0.0)
+    return why = "wpe: psd_context and regularization must be >= 0", false;
+  return true;
+}
+bool kernel_fft_supported(const gss_stft_config& s, std::string& why) {
+  const int n = s.fft_size;
+  if ((n & (n - 1)) != 0 || n < 32 || n > 4096)
+    return why = "fft_size must be a power of two in [32, 4096] on this device path", false;
+  if (s.window != 0 && s.window != 1) return why = "stft: unknown window", false;
+  return true;
+}
+
+// ---- device memory (stream-ordered pool; freed blocks are reused across batches)
+struct DevMem {
+  gss_b200_ctx* c = nullptr;
+  std::vector<std::pair<void*, size_t>> blocks;
+  cudaError_t last = cudaSuccess;
+  template <typename T>
+  T* get(size_t count) {
+    if (last != cudaSuccess) return nullptr;
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T) + 64;  // slack for aligned over-reads
+    void* p = nullptr;
+    last = cudaMallocAsync(&p, bytes, c->stream);
+    if (last != cudaSuccess) return nullptr;
+    blocks.emplace_back(p, bytes);
+    c->device_bytes += (long long)bytes;
+    return reinterpret_cast<T*>(p);
+  }
+  void release() {
+    for (auto& b : blocks) {
+      cudaFreeAsync(b.first, c->stream);
+      c->device_bytes -= (long long)b.second;
+    }
+    blocks.clear();
+  }
+};
+
+gss_status get_tables(gss_b200_ctx* c, const gss_stft_config& s, Tables& out) {
+  const auto key = std::make_pair(s.fft_size, s.window);
+  auto it = c->tables.find(key);
+  if (it != c->tables.end()) {
+    out = it->second;
+    return GSS_OK;
+  }
+  const int n = s.fft_size;
+  std::vector<float2> tw(n / 2);
+  std::vector<float> win(n);
+  for (int k = 0; k < n / 2; ++k) {
+    const double ang = -2.0 * M_PI * k / n;
+    tw[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  for (int i = 0; i < n; ++i) {  // stft.hpp:89-97
+    const double h = 0.5 * (1.0 - std::cos(2.0 * M_PI * i / n));
+    win[i] = (float)(s.window == 0 ? h : std::sqrt(h));
+  }
+  Tables t;
+  CU_TRY(c, cudaMalloc(&t.tw, sizeof(float2) * (n / 2)));
+  CU_TRY(c, cudaMalloc(&t.win, sizeof(float) * n));
+  CU_TRY(c, cudaMemcpyAsync(t.tw, tw.data(), sizeof(float2) * (n / 2), cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(t.win, win.data(), sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  c->tables[key] = t;
+  out = t;
+  return GSS_OK;
+}
+
+StftParams stft_params(const gss_stft_config& s) {
+  StftParams p;
+  p.fft_size = s.fft_size;
+  p.shift = s.shift;
+  p.window = s.window;
+  p.F = s.fft_size / 2 + 1;
+  p.log2n = ilog2(s.fft_size);
+  return p;
+}
+
+// ---- one (M, KT) group of segments and its device arrays -----------------------
+struct SegSpec {  // what the group builder needs to know about one segment
+  long long N = 0;  // audio samples (or output length for synthesis-only groups)
+  int T = 0, K = 1, target = 0, noise = -1;
+  const uint8_t* activity = nullptr;  // (T,K) or null
+  bool keep_gamma = false;
+  int index = 0;
+};
+
+struct Needs {
+  bool audio = false, y = false, yd = false, gamma = false, x = false, wave = false, em = false, wpe = false,
+       mvdr = false;
+};
+
+struct Group {
+  int M = 0, KT = 2, L = 1, F = 0, nseg = 0;
+  int max_T = 0, npat_max = 1, cell_stride = 0, max_wchunks = 1, nwork = 0, iterations = 0;
+  long long max_N = 0, nF = 0;
+  std::vector<SegDev> segs;
+  std::vector<int> members;  // caller indices
+  DevMem mem;
+  SegDev* d_segs = nullptr;
+  WorkItem* d_work = nullptr;
+  float* audio = nullptr;
+  float2 *Y = nullptr, *Yd = nullptr, *X = nullptr;
+  float *gamma = nullptr, *wave = nullptr;
+  unsigned char* pat = nullptr;
+  uint32_t* masks = nullptr;
+  float *ck = nullptr, *coef = nullptr, *part = nullptr;
+  double* cell_ll = nullptr;
+  cdbl* bstate = nullptr;
+  double *pi = nullptr, *logdet = nullptr, *bin_ll = nullptr, *seg_ll = nullptr;
+  cdbl *phi_t = nullptr, *phi_b = nullptr, *h = nullptr;
+  double* tmass = nullptr;
+  float2* hconj = nullptr;
+  float* w = nullptr;
+  float2 *gram = nullptr, *gconj = nullptr;
+  status_t* status = nullptr;
+  int *ref = nullptr, *zeroed = nullptr;
+  long long tot_audio = 0, tot_y = 0, tot_g = 0, tot_x = 0, tot_wave = 0, tot_pat = 0, tot_mask = 0;
+};
+
+int pick_chunks(gss_b200_ctx* c, int T, long long ctas_one_chunk) {
+  const int slots_mult = 64;
+  int nch = 1;
+  if (c->em_chunk_frames > 0) {
+    nch = (T + c->em_chunk_frames - 1) / c->em_chunk_frames;
+  } else if (ctas_one_chunk < 4 * 148) {
+    const int want = (int)((4 * 148 + ctas_one_chunk - 1) / ctas_one_chunk);
+    nch = std::max(1, std::min(want, (T + 255) / 256));
+  }
+  int TC = (T + nch - 1) / nch;
+  TC = ((TC + slots_mult - 1) / slots_mult) * slots_mult;
+  return std::max(TC, slots_mult);
+}
+
+gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, const std::vector<SegSpec>& specs,
+                       const Needs& need, const gss_wpe_config* wpe, int iterations) {
+  g.M = M;
+  g.KT = em_class_tier(K_for_tier);
+  g.L = em_lanes(M, g.KT);
+  g.F = F;
+  g.nseg = (int)specs.size();
+  g.iterations = iterations;
+  g.mem.c = c;
+  g.cell_stride = em_cell_floats(M, g.KT);
+  const int ndof = em_ndof(M, g.L);
+  const int km = wpe ? wpe->taps * M : 0;
+  const int wtiles = wpe ? wpe_gram_tiles(km) : 0;
+  std::vector<unsigned char> h_pat;
+  std::vector<uint32_t> h_masks;
+  long long o_audio = 0, o_y = 0, o_g = 0, o_x = 0, o_wave = 0, o_tab = 0, o_coef = 0, o_cell = 0, o_fk = 0, o_f = 0,
+            o_w = 0, o_wcell = 0, o_gw = 0;
+  for (const SegSpec& s : specs) {
+    SegDev d;
+    std::memset(&d, 0, sizeof(d));
+    d.N = (int)s.N;
+    d.T = s.T;
+    d.K = s.K;
+    d.target = s.target;
+    d.noise = s.noise;
+    d.index = s.index;
+    d.audio_off = o_audio;
+    d.y_off = o_y;
+    d.g_off = s.keep_gamma ? o_g : -1;
+    d.x_off = o_x;
+    d.wave_off = o_wave;
+    d.pat_off = (long long)h_pat.size();
+    d.mask_off = (long long)h_masks.size();
+    // activity rows -> pattern ids (first-appearance order) + class bit masks
+    if (s.activity != nullptr) {
+      std::map<uint32_t, int> seen;
+      for (int t = 0; t < s.T; ++t) {
+        uint32_t m = 0;
+        for (int k = 0; k < s.K; ++k)
+          if (s.activity[(size_t)t * s.K + k]) m |= 1u << k;
+        auto it = seen.find(m);
+        if (it == seen.end()) {
+          it = seen.emplace(m, (int)seen.size()).first;
+          h_masks.push_back(m);
+        }
+        h_pat.push_back((unsigned char)it->second);
+      }
+      d.npat = (int)seen.size();
+    } else {
+      d.npat = 0;
+    }
+    g.npat_max = std::max(g.npat_max, d.npat);
+    d.tab_off = o_tab;
+    d.coef_off = o_coef;
+    d.cell_off = o_cell;
+    d.fk_off = o_fk;
+    d.f_off = o_f;
+    d.w_off = o_w;
+    d.wcell_off = o_wcell;
+    d.g_wpe_off = o_gw;
+    d.TC = pick_chunks(c, s.T, (long long)specs.size() * F);
+    d.nchunks = (s.T + d.TC - 1) / d.TC;
+    d.WTC = c->wpe_chunk_frames > 0 ? c->wpe_chunk_frames : std::max(s.T, 1);
+    d.wchunks = (s.T + d.WTC - 1) / d.WTC;
+    d.wpe_active = (wpe != nullptr && s.T > wpe->taps + wpe->delay) ? 1 : 0;
+    g.max_wchunks = std::max(g.max_wchunks, d.wchunks);
+    g.max_T = std::max(g.max_T, s.T);
+    g.max_N = std::max(g.max_N, s.N);
+    o_audio += (long long)M * s.N;
+    o_y += (long long)F * s.T * M;
+    if (s.keep_gamma) o_g += (long long)F * s.T * s.K;
+    o_x += (long long)s.T * F;
+    o_wave += s.N;
+    o_tab += (long long)F * std::max(d.npat, 1) * g.KT;
+    o_coef += (long long)F * g.L * g.KT * ndof;
+    o_cell += (long long)F * d.nchunks;
+    o_fk += (long long)F * g.KT;
+    o_f += F;
+    o_w += (long long)F * s.T;
+    o_wcell += (long long)F * d.wchunks;
+    o_gw += (long long)F * km * M;
+    g.segs.push_back(d);
+    g.members.push_back(s.index);
+  }
+  g.nF = o_f;
+  g.tot_audio = o_audio;
+  g.tot_y = o_y;
+  g.tot_g = o_g;
+  g.tot_x = o_x;
+  g.tot_wave = o_wave;
+  g.tot_pat = (long long)h_pat.size();
+  g.tot_mask = (long long)h_masks.size();
+  std::vector<WorkItem> work;
+  for (int i = 0; i < g.nseg; ++i)
+    for (int ch = 0; ch < g.segs[i].nchunks; ++ch) work.push_back(WorkItem{i, ch});
+  g.nwork = (int)work.size();
+
+  DevMem& m = g.mem;
+  g.d_segs = m.get<SegDev>(g.nseg);
+  g.d_work = m.get<WorkItem>(work.size());
+  g.status = m.get<status_t>(g.nseg);
+  g.ref = m.get<int>(g.nseg);
+  g.zeroed = m.get<int>(g.nseg);
+  g.seg_ll = m.get<double>((size_t)g.nseg * (iterations + 1));
+  if (need.audio) g.audio = m.get<float>(o_audio);
+  if (need.y) g.Y = m.get<float2>(o_y);
+  if (need.yd) g.Yd = m.get<float2>(o_y);
+  if (need.gamma && o_g > 0) g.gamma = m.get<float>(o_g);
+  if (need.x) g.X = m.get<float2>(o_x);
+  if (need.wave) g.wave = m.get<float>(o_wave);
+  if (need.em) {
+    g.pat = m.get<unsigned char>(h_pat.size());
+    g.masks = m.get<uint32_t>(h_masks.size());
+    g.ck = m.get<float>(o_tab);
+    g.coef = m.get<float>(o_coef);
+    g.bstate = m.get<cdbl>((size_t)o_fk * M * M);
+    g.pi = m.get<double>(o_fk);
+    g.logdet = m.get<double>(o_fk);
+    g.bin_ll = m.get<double>((size_t)o_f * (iterations + 1));
+  }
+  if (need.em || need.mvdr) {
+    g.part = m.get<float>((size_t)o_cell * g.cell_stride);
+    g.cell_ll = m.get<double>(o_cell);
+  }
+  if (need.mvdr) {
+    g.phi_t = m.get<cdbl>((size_t)o_f * M * M);
+    g.phi_b = m.get<cdbl>((size_t)o_f * M * M);
+    g.tmass = m.get<double>(o_f);
+    g.h = m.get<cdbl>((size_t)o_f * M);
+    g.hconj = m.get<float2>((size_t)o_f * M);
+  }
+  if (need.wpe) {
+    g.w = m.get<float>(o_w);
+    g.gram = m.get<float2>((size_t)o_wcell * wtiles * 64);
+    g.gconj = m.get<float2>(o_gw);
+  }
+  if (m.last != cudaSuccess) {
+    const std::string why = std::string("device allocation failed: ") + cudaGetErrorString(m.last);
+    m.release();
+    return fail(c, GSS_CUDA_ERROR, why);
+  }
+  cudaStream_t st = c->stream;
+  CU_TRY(c, cudaMemcpyAsync(g.d_segs, g.segs.data(), sizeof(SegDev) * g.nseg, cudaMemcpyHostToDevice, st));
+  if (!work.empty())
+    CU_TRY(c, cudaMemcpyAsync(g.d_work, work.data(), sizeof(WorkItem) * work.size(), cudaMemcpyHostToDevice, st));
+  CU_TRY(c, cudaMemsetAsync(g.status, 0xFF, sizeof(status_t) * g.nseg, st));
+  CU_TRY(c, cudaMemsetAsync(g.zeroed, 0, sizeof(int) * g.nseg, st));
+  CU_TRY(c, cudaMemsetAsync(g.ref, 0, sizeof(int) * g.nseg, st));
+  if (need.em && !h_pat.empty()) {
+    CU_TRY(c, cudaMemcpyAsync(g.pat, h_pat.data(), h_pat.size(), cudaMemcpyHostToDevice, st));
+    CU_TRY(c, cudaMemcpyAsync(g.masks, h_masks.data(), sizeof(uint32_t) * h_masks.size(), cudaMemcpyHostToDevice, st));
+  }
+  // pageable sources above (std::vector) are consumed synchronously by cudaMemcpyAsync's
+  // staging, so they may go out of scope on return.
+  return GSS_OK;
+}
+
+// ---- stage drivers (device side only) ---------------------------------------------
+gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
+  bool any = false;
+  for (const SegDev& d : g.segs) {
+    if (d.wpe_active) {
+      any = true;
+    } else {  // pass-through (wpe.hpp:108-112)
+      CU_TRY(c, cudaMemcpyAsync(g.Yd + d.y_off, g.Y + d.y_off, sizeof(float2) * (size_t)g.F * d.T * g.M,
+                                cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  if (!any) return GSS_OK;
+  WpeArgs a;
+  a.yobs = g.Y;
+  a.yout = g.Yd;
+  a.w = g.w;
+  a.gram = g.gram;
+  a.gconj = g.gconj;
+  a.segs = g.d_segs;
+  a.status = g.status;
+  a.regularization = w.regularization;
+  a.M = g.M;
+  a.taps = w.taps;
+  a.delay = w.delay;
+  a.psd_context = w.psd_context;
+  for (int it = 0; it < w.iterations; ++it) {
+    a.ycur = it == 0 ? g.Y : g.Yd;
+    CU_TRY(c, launch_wpe_iteration(a, g.nseg, g.F, g.max_T, g.max_wchunks, c->stream, &c->launches));
+  }
+  return GSS_OK;
+}
+
+struct EmRun {
+  const float2* tensor;
+  int normalize;
+  bool final_stats;
+  bool from_state;
+  bool all_ll;  // reduce every sweep's likelihood (stage API) instead of only the last
+};
+
+gss_status run_em(gss_b200_ctx* c, Group& g, const EmRun& r) {
+  const EmShape shape{g.M, g.KT};
+  const int I = g.iterations;
+  EmUpdateArgs u;
+  u.segs = g.d_segs;
+  u.masks = g.masks;
+  u.part = g.part;
+  u.cell_ll = g.cell_ll;
+  u.bstate = g.bstate;
+  u.pi = g.pi;
+  u.logdet = g.logdet;
+  u.coef = g.coef;
+  u.ck = g.ck;
+  u.bin_ll = g.bin_ll;
+  u.status = g.status;
+  u.cell_stride = g.cell_stride;
+  u.F = g.F;
+  u.mode = r.from_state ? kEmFromState : kEmInit;
+  CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+  ++c->launches;
+  EmPassArgs p;
+  p.y = r.tensor;
+  p.segs = g.d_segs;
+  p.work = g.d_work;
+  p.pat = g.pat;
+  p.ck = g.ck;
+  p.coef = g.coef;
+  p.part = g.part;
+  p.cell_ll = g.cell_ll;
+  p.gamma = nullptr;
+  p.cell_stride = g.cell_stride;
+  p.npat_max = g.npat_max;
+  p.normalize = r.normalize;
+  for (int it = 0; it < I; ++it) {
+    CU_TRY(c, launch_em_pass(shape, false, p, g.nwork, g.F, c->stream));
+    u.mode = kEmMstep;
+    u.bin_ll = g.bin_ll + (long long)it * g.nF;
+    CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+    c->launches += 2;
+  }
+  p.gamma = g.gamma;
+  CU_TRY(c, launch_em_pass(shape, r.final_stats, p, g.nwork, g.F, c->stream));
+  u.mode = kEmFinal;
+  u.bin_ll = g.bin_ll + (long long)I * g.nF;
+  CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+  c->launches += 2;
+  for (int it = r.all_ll ? 0 : I; it <= I; ++it) {
+    CU_TRY(c, launch_sum_ll(g.bin_ll + (long long)it * g.nF, g.seg_ll + (long long)it * g.nseg, g.d_segs, g.nseg,
+                            g.F, c->stream));
+    ++c->launches;
+  }
+  return GSS_OK;
+}
+
+gss_status run_mvdr_design(gss_b200_ctx* c, Group& g, int fixed_ref, bool have_tmass) {
+  MvdrArgs a;
+  a.segs = g.d_segs;
+  a.phi_t = g.phi_t;
+  a.phi_b = g.phi_b;
+  a.tmass = have_tmass ? g.tmass : nullptr;
+  a.ref = g.ref;
+  a.zeroed = g.zeroed;
+  a.h = g.h;
+  a.hconj = g.hconj;
+  a.status = g.status;
+  a.M = g.M;
+  a.F = g.F;
+  a.fixed_ref = fixed_ref;
+  CU_TRY(c, launch_select_reference(a, g.nseg, c->stream));
+  CU_TRY(c, launch_mvdr_solve(a, g.nseg, c->stream));
+  c->launches += 2;
+  return GSS_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// batch object
+// ===========================================================================
+struct gss_b200_batch {
+  gss_pipeline_config cfg;
+  int n = 0;
+  std::vector<gss_segment_desc> desc;
+  std::vector<std::vector<int64_t>> pb, pe;
+  std::vector<Fail> fails;           // per segment host-side verdicts (code 0 = ok)
+  std::vector<int> frames;
+  std::vector<std::unique_ptr<Group>> groups;
+  std::vector<cudaEvent_t> events;   // 6 per group + 2 around upload
+  bool ran = false;
+  Tables tables;
+};
+
+namespace {
+
+void free_batch(gss_b200_ctx* c, gss_b200_batch* b) {
+  if (!b) return;
+  for (auto& g : b->groups) g->mem.release();
+  for (cudaEvent_t e : b->events) cudaEventDestroy(e);
+  delete b;
+  (void)c;
+}
+
+}  // namespace
+
+extern "C" {
+
+void gss_b200_default_stft_config(gss_stft_config* c) {
+  c->fft_size = 1024;
+  c->shift = 256;
+  c->window = 0;
+  c->sample_rate = 16000;
+}
+void gss_b200_default_wpe_config(gss_wpe_config* c) {
+  c->taps = 10;
+  c->delay = 2;
+  c->iterations = 3;
+  c->psd_context = 0;
+  c->regularization = 1e-10;
+}
+void gss_b200_default_pipeline_config(gss_pipeline_config* c) {
+  gss_b200_default_stft_config(&c->stft);
+  gss_b200_default_wpe_config(&c->wpe);
+  c->enable_wpe = 1;
+  c->bss_iterations = 20;
+}
+
+gss_status gss_b200_create(int device, gss_b200_ctx** out) {
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count <= 0)
+    return fail(nullptr, GSS_CUDA_ERROR,
+                std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                    "); libgss_b200 has no CPU fallback");
+  if (device < 0 || device >= count) return fail(nullptr, GSS_CUDA_ERROR, "device index out of range");
+  CU_TRY(nullptr, cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CU_TRY(nullptr, cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(nullptr, GSS_CUDA_ERROR, "libgss_b200 is built for sm_100a (B200) only");
+  auto* c = new gss_b200_ctx();
+  c->device = device;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(nullptr, GSS_CUDA_ERROR, cudaGetErrorString(e));
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long thr = ~0ull;  // keep freed blocks cached for the next batch
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (const char* s = std::getenv("GSS_B200_EM_CHUNK_FRAMES")) c->em_chunk_frames = std::atoi(s);
+  if (const char* s = std::getenv("GSS_B200_WPE_CHUNK_FRAMES")) c->wpe_chunk_frames = std::atoi(s);
+  *out = c;
+  return GSS_OK;
+}
+
+void gss_b200_destroy(gss_b200_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->tables) {
+    cudaFree(kv.second.tw);
+    cudaFree(kv.second.win);
+  }
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* gss_b200_last_error(const gss_b200_ctx* c) { return c ? c->err.c_str() : t_err.c_str(); }
+int64_t gss_b200_last_error_frequency(const gss_b200_ctx* c) { return c ? c->err_freq : t_err_freq; }
+void* gss_b200_stream(gss_b200_ctx* c) { return c ? (void*)c->stream : nullptr; }
+int64_t gss_b200_launch_count(const gss_b200_ctx* c) { return c ? c->launches : 0; }
+int64_t gss_b200_device_bytes(const gss_b200_ctx* c) { return c ? c->device_bytes : 0; }
+
+gss_status gss_b200_host_alloc(int64_t bytes, void** out) {
+  *out = nullptr;
+  cudaError_t e = cudaMallocHost(out, (size_t)std::max<int64_t>(bytes, 1));
+  if (e != cudaSuccess) return fail(nullptr, GSS_CUDA_ERROR, cudaGetErrorString(e));
+  return GSS_OK;
+}
+void gss_b200_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+gss_status gss_b200_stage_ms(gss_b200_ctx* c, double* ms) {
+  for (int i = 0; i < GSS_B200_NUM_STAGES; ++i) ms[i] = c->stage_ms[i];
+  return GSS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// enhance_batch = upload + run + fetch
+// ---------------------------------------------------------------------------
+gss_status gss_b200_batch_upload(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
+                                 const gss_pipeline_config* cfg, gss_b200_batch** out) {
+  *out = nullptr;
+  if (!c) return fail(nullptr, GSS_INTERNAL_ERROR, "null context");
+  CU_TRY(c, cudaSetDevice(c->device));
+  std::string why;
+  // same order as PipelineConfig::validate (scheduler.hpp:46-57)
+  if (cfg->bss_iterations < 1) return fail(c, GSS_CONFIG_ERROR, "scheduler: bss_iterations must be >= 1");
+  if (!validate_wpe(cfg->wpe, why)) return fail(c, GSS_CONFIG_ERROR, why);
+  if (!validate_stft(cfg->stft, why)) return fail(c, GSS_CONFIG_ERROR, why);
+  if (!kernel_fft_supported(cfg->stft, why)) return fail(c, GSS_UNSUPPORTED, why);
+  if (n < 0) return fail(c, GSS_SHAPE_ERROR, "negative segment count");
+  auto* b = new gss_b200_batch();
+  b->cfg = *cfg;
+  b->n = n;
+  b->desc.assign(segs, segs + n);
+  b->pb.resize(n);
+  b->pe.resize(n);
+  b->fails.assign(n, Fail{GSS_OK, "", -1});
+  b->frames.assign(n, 0);
+  gss_status rc = get_tables(c, cfg->stft, b->tables);
+  if (rc != GSS_OK) {
+    delete b;
+    return rc;
+  }
+  const int F = cfg->stft.fft_size / 2 + 1;
+  // host-side validation per segment, in the order the reference would raise
+  std::map<std::pair<int, int>, std::vector<SegSpec>> by_shape;
+  for (int i = 0; i < n; ++i) {
+    const gss_segment_desc& d = b->desc[i];
+    Fail& fl = b->fails[i];
+    b->pb[i].assign(d.part_begin, d.part_begin + std::max(d.num_parts, 0));
+    b->pe[i].assign(d.part_end, d.part_end + std::max(d.num_parts, 0));
+    if (d.channels < 1) {
+      fl = Fail{GSS_SHAPE_ERROR, "stft.analyze: no channels", -1};
+    } else if (d.num_samples < cfg->stft.fft_size) {
+      fl = Fail{GSS_INPUT_TOO_SHORT_ERROR, "stft.analyze: fewer samples than fft_size", -1};
+    } else if (d.sample_rate > 0 && d.sample_rate != cfg->stft.sample_rate) {
+      fl = Fail{GSS_CONFIG_ERROR, "stft.analyze: signal/config sample rate mismatch", -1};
+    } else if (d.channels > kMaxChannels || d.num_classes > kMaxClasses) {
+      fl = Fail{GSS_UNSUPPORTED, "more than 8 channels or classes", -1};
+    } else if (d.num_samples > 0x7fffffffLL) {
+      fl = Fail{GSS_UNSUPPORTED, "segment longer than 2^31 samples", -1};
+    }
+    if (fl.code != GSS_OK) continue;
+    const int64_t T = gss_b200_frame_count(d.num_samples, cfg->stft.fft_size, cfg->stft.shift);
+    b->frames[i] = (int)T;
+    if (d.activity_frames != T) {
+      fl = Fail{GSS_SHAPE_ERROR, "cacgmm: activity frames do not match tensor", -1};
+    } else if (d.num_classes < 1 || d.target_index < 0 || d.target_index >= d.num_classes) {
+      fl = Fail{GSS_SHAPE_ERROR, "accumulate_stats: target class out of range", -1};
+    } else {
+      for (int p = 0; p < d.num_parts; ++p)
+        if (b->pb[i][p] < 0 || b->pb[i][p] > std::min<int64_t>(b->pe[i][p], d.num_samples))
+          fl = Fail{GSS_SHAPE_ERROR, "part offsets outside the assembled audio", -1};
+    }
+    if (fl.code != GSS_OK) continue;
+    SegSpec s;
+    s.N = d.num_samples;
+    s.T = (int)T;
+    s.K = d.num_classes;
+    s.target = d.target_index;
+    s.noise = d.noise_index;
+    s.activity = d.activity;
+    s.keep_gamma = d.gamma_out != nullptr;
+    s.index = i;
+    by_shape[std::make_pair(d.channels, em_class_tier(d.num_classes))].push_back(s);
+  }
+  b->events.resize(2 + 6 * by_shape.size());
+  for (auto& e : b->events) cudaEventCreate(&e);
+  cudaEventRecord(b->events[0], c->stream);
+  Needs need;
+  need.audio = need.y = need.x = need.wave = need.em = need.mvdr = true;
+  need.yd = need.wpe = cfg->enable_wpe != 0;
+  need.gamma = true;
+  for (auto& kv : by_shape) {
+    std::unique_ptr<Group> g(new Group());
+    rc = build_group(c, *g, kv.first.first, kv.first.second, F, kv.second, need,
+                     cfg->enable_wpe ? &cfg->wpe : nullptr, cfg->bss_iterations);
+    if (rc != GSS_OK) {
+      g->mem.release();
+      free_batch(c, b);
+      return rc;
+    }
+    for (int j = 0; j < g->nseg; ++j) {
+      const gss_segment_desc& d = b->desc[g->members[j]];
+      cudaError_t e = cudaMemcpyAsync(g->audio + g->segs[j].audio_off, d.audio,
+                                      sizeof(float) * (size_t)d.channels * d.num_samples, cudaMemcpyHostToDevice,
+                                      c->stream);
+      if (e != cudaSuccess) {
+        g->mem.release();
+        free_batch(c, b);
+        return fail(c, GSS_CUDA_ERROR, cudaGetErrorString(e));
+      }
+    }
+    b->groups.push_back(std::move(g));
+  }
+  cudaEventRecord(b->events[1], c->stream);
+  *out = b;
+  return GSS_OK;
+}
+
+gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) {
+  CU_TRY(c, cudaSetDevice(c->device));
+  const gss_pipeline_config& cfg = b->cfg;
+  const StftParams sp = stft_params(cfg.stft);
+  int gi = 0;
+  for (auto& gp : b->groups) {
+    Group& g = *gp;
+    cudaEvent_t* ev = &b->events[2 + 6 * gi++];
+    cudaStream_t st = c->stream;
+    // device-side state that a previous run of the same batch may have touched
+    CU_TRY(c, cudaMemsetAsync(g.status, 0xFF, sizeof(status_t) * g.nseg, st));
+    CU_TRY(c, cudaMemsetAsync(g.zeroed, 0, sizeof(int) * g.nseg, st));
+    cudaEventRecord(ev[0], st);
+    {
+      StftArgs a;
+      a.audio = g.audio;
+      a.y = g.Y;
+      a.segs = g.d_segs;
+      a.tw = b->tables.tw;
+      a.win = b->tables.win;
+      a.p = sp;
+      a.M = g.M;
+      a.TB = 0;
+      CU_TRY(c, launch_stft(a, g.nseg, g.max_T, st));
+      ++c->launches;
+    }
+    cudaEventRecord(ev[1], st);
+    const float2* tensor = g.Y;
+    if (cfg.enable_wpe) {
+      gss_status rc = run_wpe(c, g, cfg.wpe);
+      if (rc != GSS_OK) return rc;
+      tensor = g.Yd;
+    }
+    cudaEventRecord(ev[2], st);
+    {
+      EmRun r{tensor, 1, true, false, false};
+      gss_status rc = run_em(c, g, r);
+      if (rc != GSS_OK) return rc;
+    }
+    cudaEventRecord(ev[3], st);
+    {
+      StatsFinalArgs sf;
+      sf.segs = g.d_segs;
+      sf.part = g.part;
+      sf.phi_t = g.phi_t;
+      sf.phi_b = g.phi_b;
+      sf.tmass = g.tmass;
+      sf.cell_stride = g.cell_stride;
+      sf.F = g.F;
+      CU_TRY(c, launch_mvdr_stats_final(EmShape{g.M, g.KT}, sf, g.nseg, st));
+      ++c->launches;
+      gss_status rc = run_mvdr_design(c, g, -1, true);
+      if (rc != GSS_OK) return rc;
+      ApplyArgs aa;
+      aa.y = tensor;
+      aa.hconj = g.hconj;
+      aa.x = g.X;
+      aa.segs = g.d_segs;
+      aa.M = g.M;
+      aa.F = g.F;
+      aa.frame_major = 1;
+      CU_TRY(c, launch_apply(aa, g.nseg, g.max_T, st));
+      ++c->launches;
+    }
+    cudaEventRecord(ev[4], st);
+    {
+      IstftArgs ia;
+      ia.x = g.X;
+      ia.wave = g.wave;
+      ia.segs = g.d_segs;
+      ia.tw = b->tables.tw;
+      ia.win = b->tables.win;
+      ia.p = sp;
+      ia.HB = 0;
+      CU_TRY(c, launch_istft(ia, g.nseg, g.max_N, st));
+      ++c->launches;
+    }
+    cudaEventRecord(ev[5], st);
+  }
+  b->ran = true;
+  return GSS_OK;
+}
+
+gss_status gss_b200_batch_fetch(gss_b200_ctx* c, gss_b200_batch* b, gss_segment_diag* diags) {
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (!b->ran) return fail(c, GSS_INTERNAL_ERROR, "batch_fetch before batch_run");
+  cudaStream_t st = c->stream;
+  const int F = b->cfg.stft.fft_size / 2 + 1;
+  const int I = b->cfg.bss_iterations;
+  for (int i = 0; i < b->n; ++i) {
+    diags[i].status = b->fails[i].code;
+    diags[i].ref_channel = 0;
+    diags[i].error_frequency = b->fails[i].freq;
+    diags[i].zeroed_bins = 0;
+    diags[i].frames = b->frames[i];
+    diags[i].ll_final = 0.0;
+    for (int p = 0; p < b->desc[i].num_parts; ++p) b->desc[i].out_lengths[p] = 0;
+  }
+  cudaEvent_t d2h0, d2h1;
+  cudaEventCreate(&d2h0);
+  cudaEventCreate(&d2h1);
+  cudaEventRecord(d2h0, st);
+  // small per-segment results first (they decide which waveforms are copied)
+  struct Small {
+    std::vector<status_t> status;
+    std::vector<int> ref, zeroed;
+    std::vector<double> ll;
+  };
+  std::vector<Small> small(b->groups.size());
+  for (size_t gi = 0; gi < b->groups.size(); ++gi) {
+    Group& g = *b->groups[gi];
+    Small& s = small[gi];
+    s.status.resize(g.nseg);
+    s.ref.resize(g.nseg);
+    s.zeroed.resize(g.nseg);
+    s.ll.resize(g.nseg);
+    CU_TRY(c, cudaMemcpyAsync(s.status.data(), g.status, sizeof(status_t) * g.nseg, cudaMemcpyDeviceToHost, st));
+    CU_TRY(c, cudaMemcpyAsync(s.ref.data(), g.ref, sizeof(int) * g.nseg, cudaMemcpyDeviceToHost, st));
+    CU_TRY(c, cudaMemcpyAsync(s.zeroed.data(), g.zeroed, sizeof(int) * g.nseg, cudaMemcpyDeviceToHost, st));
+    CU_TRY(c, cudaMemcpyAsync(s.ll.data(), g.seg_ll + (long long)I * g.nseg, sizeof(double) * g.nseg,
+                              cudaMemcpyDeviceToHost, st));
+  }
+  CU_TRY(c, cudaStreamSynchronize(st));
+  for (size_t gi = 0; gi < b->groups.size(); ++gi) {
+    Group& g = *b->groups[gi];
+    const Small& s = small[gi];
+    for (int j = 0; j < g.nseg; ++j) {
+      const int i = g.members[j];
+      const gss_segment_desc& d = b->desc[i];
+      gss_segment_diag& dg = diags[i];
+      dg.ref_channel = s.ref[j];
+      dg.zeroed_bins = s.zeroed[j];
+      dg.ll_final = s.ll[j];
+      if (s.status[j] != kStatusOk) {
+        dg.status = (int)(s.status[j] >> 32);
+        dg.error_frequency = dg.status == GSS_SINGULAR_MATRIX_ERROR ? (int64_t)(s.status[j] & 0xffffffffu) : -1;
+        b->fails[i] = Fail{(gss_status)dg.status,
+                           dg.status == GSS_DEGENERATE_STATS_ERROR ? "accumulate_stats: target mask is all zero"
+                                                                   : "matrix has no positive eigenvalue",
+                           dg.error_frequency};
+        continue;
+      }
+      const SegDev& sd = g.segs[j];
+      int64_t off = 0;
+      for (int p = 0; p < d.num_parts; ++p) {
+        const int64_t hi = std::min<int64_t>(b->pe[i][p], d.num_samples);  // scheduler.hpp:354-356
+        const int64_t len = hi - b->pb[i][p];
+        if (len > 0)
+          CU_TRY(c, cudaMemcpyAsync(d.out_wave + off, g.wave + sd.wave_off + b->pb[i][p], sizeof(float) * len,
+                                    cudaMemcpyDeviceToHost, st));
+        d.out_lengths[p] = len;
+        off += len;
+      }
+      if (d.mono_out)
+        CU_TRY(c, cudaMemcpyAsync(d.mono_out, g.wave + sd.wave_off, sizeof(float) * d.num_samples,
+                                  cudaMemcpyDeviceToHost, st));
+      if (d.gamma_out && sd.g_off >= 0)
+        CU_TRY(c, cudaMemcpyAsync(d.gamma_out, g.gamma + sd.g_off, sizeof(float) * (size_t)F * sd.T * sd.K,
+                                  cudaMemcpyDeviceToHost, st));
+      if (d.h_out)
+        CU_TRY(c, cudaMemcpyAsync(d.h_out, g.h + sd.f_off * g.M, sizeof(cdbl) * (size_t)F * g.M,
+                                  cudaMemcpyDeviceToHost, st));
+    }
+  }
+  cudaEventRecord(d2h1, st);
+  CU_TRY(c, cudaStreamSynchronize(st));
+  // stage clocks
+  for (double& v : c->stage_ms) v = 0.0;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, b->events[0], b->events[1]) == cudaSuccess) c->stage_ms[5] = ms;
+  if (cudaEventElapsedTime(&ms, d2h0, d2h1) == cudaSuccess) c->stage_ms[6] = ms;
+  for (size_t gi = 0; gi < b->groups.size(); ++gi)
+    for (int s = 0; s < 5; ++s)
+      if (cudaEventElapsedTime(&ms, b->events[2 + 6 * gi + s], b->events[2 + 6 * gi + s + 1]) == cudaSuccess)
+        c->stage_ms[s] += ms;
+  cudaEventDestroy(d2h0);
+  cudaEventDestroy(d2h1);
+  // remember the first failure for gss_b200_last_error
+  for (int i = 0; i < b->n; ++i)
+    if (b->fails[i].code != GSS_OK) {
+      c->err = std::string(status_name(b->fails[i].code)) + ": " + b->fails[i].msg + " (segment " +
+               std::to_string(i) + ")";
+      c->err_freq = b->fails[i].freq;
+      break;
+    }
+  return GSS_OK;
+}
+
+void gss_b200_batch_free(gss_b200_ctx* c, gss_b200_batch* b) {
+  if (c) cudaSetDevice(c->device);
+  free_batch(c, b);
+}
+
+gss_status gss_b200_enhance_batch(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
+                                  const gss_pipeline_config* cfg, gss_segment_diag* diags) {
+  gss_b200_batch* b = nullptr;
+  gss_status rc = gss_b200_batch_upload(c, n, segs, cfg, &b);
+  if (rc != GSS_OK) return rc;
+  rc = gss_b200_batch_run(c, b);
+  if (rc == GSS_OK) rc = gss_b200_batch_fetch(c, b, diags);
+  cudaStreamSynchronize(c->stream);
+  gss_b200_batch_free(c, b);
+  return rc;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// stage entry points: one tensor per call, through the same kernels
+// ===========================================================================
+namespace {
+
+struct StageGroup {
+  gss_b200_ctx* c;
+  Group g;
+  explicit StageGroup(gss_b200_ctx* ctx) : c(ctx) {}
+  ~StageGroup() {
+    cudaStreamSynchronize(c->stream);
+    g.mem.release();
+  }
+};
+
+gss_status check_tensor(gss_b200_ctx* c, int bins, int64_t frames, int channels) {
+  if (!c) return fail(nullptr, GSS_INTERNAL_ERROR, "null context");
+  if (bins < 1 || frames < 1 || channels < 1) return fail(c, GSS_SHAPE_ERROR, "empty tensor");
+  if (channels > kMaxChannels) return fail(c, GSS_UNSUPPORTED, "more than 8 channels");
+  if (frames > 0x7fffffffLL / std::max(1, channels)) return fail(c, GSS_UNSUPPORTED, "too many frames");
+  return GSS_OK;
+}
+
+gss_status device_status(gss_b200_ctx* c, Group& g) {
+  status_t s = kStatusOk;
+  CU_TRY(c, cudaMemcpyAsync(&s, g.status, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (s == kStatusOk) return GSS_OK;
+  const int code = (int)(s >> 32);
+  if (code == GSS_SINGULAR_MATRIX_ERROR)
+    return fail(c, GSS_SINGULAR_MATRIX_ERROR, "matrix has no positive eigenvalue", (long long)(s & 0xffffffffu));
+  if (code == GSS_DEGENERATE_STATS_ERROR)
+    return fail(c, GSS_DEGENERATE_STATS_ERROR, "accumulate_stats: target mask is all zero");
+  return fail(c, (gss_status)code, "device-side failure");
+}
+
+}  // namespace
+
+extern "C" {
+
+gss_status gss_b200_stft(gss_b200_ctx* c, const float* audio, int32_t M, int64_t N, int32_t signal_rate,
+                         const gss_stft_config* cfg, float* out) {
+  if (!c) return fail(nullptr, GSS_INTERNAL_ERROR, "null context");
+  CU_TRY(c, cudaSetDevice(c->device));
+  std::string why;
+  if (!validate_stft(*cfg, why)) return fail(c, GSS_CONFIG_ERROR, why);
+  if (M < 1) return fail(c, GSS_SHAPE_ERROR, "stft.analyze: no channels");
+  if (N < cfg->fft_size) return fail(c, GSS_INPUT_TOO_SHORT_ERROR, "stft.analyze: fewer samples than fft_size");
+  if (signal_rate > 0 && signal_rate != cfg->sample_rate)
+    return fail(c, GSS_CONFIG_ERROR, "stft.analyze: signal/config sample rate mismatch");
+  if (!kernel_fft_supported(*cfg, why)) return fail(c, GSS_UNSUPPORTED, why);
+  if (M > kMaxChannels || N > 0x7fffffffLL) return fail(c, GSS_UNSUPPORTED, "more than 8 channels");
+  Tables tb;
+  gss_status rc = get_tables(c, *cfg, tb);
+  if (rc != GSS_OK) return rc;
+  const int F = cfg->fft_size / 2 + 1;
+  const int64_t T = gss_b200_frame_count(N, cfg->fft_size, cfg->shift);
+  StageGroup sg(c);
+  SegSpec s;
+  s.N = N;
+  s.T = (int)T;
+  Needs need;
+  need.audio = need.y = true;
+  rc = build_group(c, sg.g, M, 1, F, {s}, need, nullptr, 0);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaMemcpyAsync(sg.g.audio, audio, sizeof(float) * (size_t)M * N, cudaMemcpyHostToDevice, c->stream));
+  StftArgs a;
+  a.audio = sg.g.audio;
+  a.y = sg.g.Y;
+  a.segs = sg.g.d_segs;
+  a.tw = tb.tw;
+  a.win = tb.win;
+  a.p = stft_params(*cfg);
+  a.M = M;
+  a.TB = 0;
+  CU_TRY(c, launch_stft(a, 1, (int)T, c->stream));
+  ++c->launches;
+  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Y, sizeof(float2) * (size_t)F * T * M, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return GSS_OK;
+}
+
+gss_status gss_b200_istft(gss_b200_ctx* c, const float* spec, int32_t bins, int64_t T, int32_t M,
+                          int64_t num_samples, const gss_stft_config* cfg, float* out) {
+  gss_status rc = check_tensor(c, bins, T, M);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  std::string why;
+  if (!validate_stft(*cfg, why)) return fail(c, GSS_CONFIG_ERROR, why);
+  if (bins != cfg->fft_size / 2 + 1) return fail(c, GSS_CONFIG_ERROR, "stft.synthesize: tensor bins do not match config");
+  if (!kernel_fft_supported(*cfg, why)) return fail(c, GSS_UNSUPPORTED, why);
+  Tables tb;
+  rc = get_tables(c, *cfg, tb);
+  if (rc != GSS_OK) return rc;
+  const int F = bins;
+  const int64_t padded_len = (T - 1) * cfg->shift + cfg->fft_size;
+  const int64_t out_len = num_samples > 0 ? num_samples : std::max<int64_t>(0, padded_len - cfg->fft_size);
+  if (out_len == 0) return GSS_OK;
+  if (out_len > 0x7fffffffLL) return fail(c, GSS_UNSUPPORTED, "output longer than 2^31 samples");
+  StageGroup sg(c);
+  SegSpec s;
+  s.N = out_len;
+  s.T = (int)T;
+  Needs need;
+  need.y = need.x = need.wave = need.mvdr = true;
+  rc = build_group(c, sg.g, M, 1, F, {s}, need, nullptr, 0);
+  if (rc != GSS_OK) return rc;
+  Group& g = sg.g;
+  CU_TRY(c, cudaMemcpyAsync(g.Y, spec, sizeof(float2) * (size_t)F * T * M, cudaMemcpyHostToDevice, c->stream));
+  std::vector<float2> sel((size_t)F * M);
+  for (int ch = 0; ch < M; ++ch) {
+    // channel selection through the beamformer kernel: h = e_ch
+    for (int f = 0; f < F; ++f)
+      for (int m = 0; m < M; ++m) sel[(size_t)f * M + m] = make_float2(m == ch ? 1.f : 0.f, 0.f);
+    CU_TRY(c, cudaMemcpyAsync(g.hconj, sel.data(), sizeof(float2) * sel.size(), cudaMemcpyHostToDevice, c->stream));
+    ApplyArgs aa;
+    aa.y = g.Y;
+    aa.hconj = g.hconj;
+    aa.x = g.X;
+    aa.segs = g.d_segs;
+    aa.M = M;
+    aa.F = F;
+    aa.frame_major = 1;
+    CU_TRY(c, launch_apply(aa, 1, (int)T, c->stream));
+    IstftArgs ia;
+    ia.x = g.X;
+    ia.wave = g.wave;
+    ia.segs = g.d_segs;
+    ia.tw = tb.tw;
+    ia.win = tb.win;
+    ia.p = stft_params(*cfg);
+    ia.HB = 0;
+    CU_TRY(c, launch_istft(ia, 1, out_len, c->stream));
+    c->launches += 2;
+    CU_TRY(c, cudaMemcpyAsync(out + (size_t)ch * out_len, g.wave, sizeof(float) * out_len, cudaMemcpyDeviceToHost,
+                              c->stream));
+    CU_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  return GSS_OK;
+}
+
+gss_status gss_b200_wpe(gss_b200_ctx* c, const float* in, int32_t bins, int64_t T, int32_t M,
+                        const gss_wpe_config* cfg, float* out) {
+  gss_status rc = check_tensor(c, bins, T, M);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  std::string why;
+  if (!validate_wpe(*cfg, why)) return fail(c, GSS_CONFIG_ERROR, why);
+  const size_t bytes = sizeof(float2) * (size_t)bins * T * M;
+  if (T <= cfg->taps + cfg->delay) {  // wpe.hpp:108-112: input returned unchanged
+    if (out != in) std::memmove(out, in, bytes);
+    return GSS_OK;
+  }
+  StageGroup sg(c);
+  SegSpec s;
+  s.T = (int)T;
+  Needs need;
+  need.y = need.yd = need.wpe = true;
+  rc = build_group(c, sg.g, M, 1, bins, {s}, need, cfg, 0);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaMemcpyAsync(sg.g.Y, in, bytes, cudaMemcpyHostToDevice, c->stream));
+  rc = run_wpe(c, sg.g, *cfg);
+  if (rc != GSS_OK) return rc;
+  rc = device_status(c, sg.g);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Yd, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return GSS_OK;
+}
+
+gss_status gss_b200_unit_normalize(gss_b200_ctx* c, const float* in, int32_t bins, int64_t T, int32_t M,
+                                   float* out) {
+  gss_status rc = check_tensor(c, bins, T, M);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  StageGroup sg(c);
+  SegSpec s;
+  s.T = (int)T;
+  Needs need;
+  need.y = need.yd = true;
+  rc = build_group(c, sg.g, M, 1, bins, {s}, need, nullptr, 0);
+  if (rc != GSS_OK) return rc;
+  const size_t bytes = sizeof(float2) * (size_t)bins * T * M;
+  CU_TRY(c, cudaMemcpyAsync(sg.g.Y, in, bytes, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, launch_unit_normalize(sg.g.Y, sg.g.Yd, (long long)bins * T, M, c->stream));
+  ++c->launches;
+  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Yd, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return GSS_OK;
+}
+
+static gss_status em_common(gss_b200_ctx* c, const float* yn, int32_t bins, int64_t T, int32_t M,
+                            const uint8_t* act, int64_t act_frames, int32_t K, int32_t noise, int32_t iterations,
+                            const double* pi_in, const double* shapes_in, float* gamma, double* pi,
+                            double* shapes, double* trace) {
+  gss_status rc = check_tensor(c, bins, T, M);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  const bool from_state = pi_in != nullptr;
+  if (!from_state && iterations < 1) return fail(c, GSS_CONFIG_ERROR, "cacgmm: iterations must be >= 1");
+  if (act_frames != T) return fail(c, GSS_SHAPE_ERROR, "cacgmm: activity frames do not match tensor");
+  if (K < 1) return fail(c, GSS_SHAPE_ERROR, "cacgmm: no classes");
+  if (K > kMaxClasses) return fail(c, GSS_UNSUPPORTED, "more than 8 classes");
+  StageGroup sg(c);
+  SegSpec s;
+  s.T = (int)T;
+  s.K = K;
+  s.noise = noise;
+  s.activity = act;
+  s.keep_gamma = gamma != nullptr;
+  Needs need;
+  need.y = need.em = need.gamma = true;
+  rc = build_group(c, sg.g, M, K, bins, {s}, need, nullptr, from_state ? 0 : iterations);
+  if (rc != GSS_OK) return rc;
+  Group& g = sg.g;
+  const int KT = g.KT, MM = M * M;
+  CU_TRY(c, cudaMemcpyAsync(g.Y, yn, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyHostToDevice, c->stream));
+  std::vector<double> h_pi;
+  std::vector<cdbl> h_b;
+  if (from_state) {
+    h_pi.assign((size_t)bins * KT, 0.0);
+    h_b.assign((size_t)bins * KT * MM, cd_make(0.0, 0.0));
+    for (int f = 0; f < bins; ++f)
+      for (int k = 0; k < K; ++k) {
+        h_pi[(size_t)f * KT + k] = pi_in[(size_t)f * K + k];
+        for (int i = 0; i < MM; ++i)
+          h_b[((size_t)f * KT + k) * MM + i] = cd_make(shapes_in[2 * (((size_t)f * K + k) * MM + i)],
+                                                        shapes_in[2 * (((size_t)f * K + k) * MM + i) + 1]);
+      }
+    CU_TRY(c, cudaMemcpyAsync(g.pi, h_pi.data(), sizeof(double) * h_pi.size(), cudaMemcpyHostToDevice, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(g.bstate, h_b.data(), sizeof(cdbl) * h_b.size(), cudaMemcpyHostToDevice, c->stream));
+  }
+  EmRun r{g.Y, 0, false, from_state, true};
+  rc = run_em(c, g, r);
+  if (rc != GSS_OK) return rc;
+  rc = device_status(c, g);
+  if (rc != GSS_OK) return rc;
+  const int I = g.iterations;
+  if (gamma)
+    CU_TRY(c, cudaMemcpyAsync(gamma, g.gamma, sizeof(float) * (size_t)bins * T * K, cudaMemcpyDeviceToHost, c->stream));
+  if (trace) CU_TRY(c, cudaMemcpyAsync(trace, g.seg_ll, sizeof(double) * (I + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (pi || shapes) {
+    h_pi.resize((size_t)bins * KT);
+    h_b.resize((size_t)bins * KT * MM);
+    CU_TRY(c, cudaMemcpyAsync(h_pi.data(), g.pi, sizeof(double) * h_pi.size(), cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(h_b.data(), g.bstate, sizeof(cdbl) * h_b.size(), cudaMemcpyDeviceToHost, c->stream));
+  }
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  if (pi || shapes)
+    for (int f = 0; f < bins; ++f)
+      for (int k = 0; k < K; ++k) {  // drop the class padding of the kernel tier
+        if (pi) pi[(size_t)f * K + k] = h_pi[(size_t)f * KT + k];
+        if (shapes)
+          std::memcpy(shapes + 2 * (((size_t)f * K + k) * MM), &h_b[((size_t)f * KT + k) * MM], sizeof(cdbl) * MM);
+      }
+  return GSS_OK;
+}
+
+gss_status gss_b200_em_fit(gss_b200_ctx* c, const float* yn, int32_t bins, int64_t T, int32_t M,
+                           const uint8_t* act, int64_t act_frames, int32_t K, int32_t noise, int32_t iterations,
+                           float* gamma, double* pi, double* shapes, double* trace) {
+  return em_common(c, yn, bins, T, M, act, act_frames, K, noise, iterations, nullptr, nullptr, gamma, pi, shapes,
+                   trace);
+}
+
+gss_status gss_b200_log_likelihood(gss_b200_ctx* c, const float* yn, int32_t bins, int64_t T, int32_t M,
+                                   const uint8_t* act, int32_t K, int32_t noise, const double* pi,
+                                   const double* shapes, double* out) {
+  if (!pi || !shapes) return fail(c, GSS_SHAPE_ERROR, "log_likelihood: inconsistent shapes");
+  return em_common(c, yn, bins, T, M, act, T, K, noise, 0, pi, shapes, nullptr, nullptr, nullptr, out);
+}
+
+gss_status gss_b200_mvdr_stats(gss_b200_ctx* c, const float* y, const float* gamma, int32_t bins, int64_t T,
+                               int32_t M, int32_t K, int32_t target, double* tgt, double* bg) {
+  gss_status rc = check_tensor(c, bins, T, M);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (K < 1 || K > kMaxClasses) return fail(c, K < 1 ? GSS_SHAPE_ERROR : GSS_UNSUPPORTED, "class count out of range");
+  if (target < 0 || target >= K) return fail(c, GSS_SHAPE_ERROR, "accumulate_stats: target class out of range");
+  StageGroup sg(c);
+  SegSpec s;
+  s.T = (int)T;
+  s.K = K;
+  s.target = target;
+  s.keep_gamma = true;
+  Needs need;
+  need.y = need.gamma = need.mvdr = true;
+  rc = build_group(c, sg.g, M, K, bins, {s}, need, nullptr, 0);
+  if (rc != GSS_OK) return rc;
+  Group& g = sg.g;
+  CU_TRY(c, cudaMemcpyAsync(g.Y, y, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.gamma, gamma, sizeof(float) * (size_t)bins * T * K, cudaMemcpyHostToDevice, c->stream));
+  StatsPassArgs sp;
+  sp.y = g.Y;
+  sp.gamma = g.gamma;
+  sp.segs = g.d_segs;
+  sp.work = g.d_work;
+  sp.part = g.part;
+  sp.cell_stride = g.cell_stride;
+  CU_TRY(c, launch_mvdr_stats(EmShape{g.M, g.KT}, sp, g.nwork, bins, c->stream));
+  StatsFinalArgs sf;
+  sf.segs = g.d_segs;
+  sf.part = g.part;
+  sf.phi_t = g.phi_t;
+  sf.phi_b = g.phi_b;
+  sf.tmass = g.tmass;
+  sf.cell_stride = g.cell_stride;
+  sf.F = bins;
+  CU_TRY(c, launch_mvdr_stats_final(EmShape{g.M, g.KT}, sf, 1, c->stream));
+  c->launches += 2;
+  std::vector<double> tm(bins);
+  CU_TRY(c, cudaMemcpyAsync(tm.data(), g.tmass, sizeof(double) * bins, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(tgt, g.phi_t, sizeof(cdbl) * (size_t)bins * M * M, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(bg, g.phi_b, sizeof(cdbl) * (size_t)bins * M * M, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  double total = 0.0;
+  for (double v : tm) total += v;
+  if (total <= 0.0) return fail(c, GSS_DEGENERATE_STATS_ERROR, "accumulate_stats: target mask is all zero");
+  return GSS_OK;
+}
+
+static gss_status mvdr_common(gss_b200_ctx* c, const double* tgt, const double* bg, int32_t bins, int32_t M,
+                              int fixed_ref, int32_t* ref_out, double* h, int64_t* zeroed) {
+  gss_status rc = check_tensor(c, bins, 1, M);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  StageGroup sg(c);
+  SegSpec s;
+  s.T = 1;
+  Needs need;
+  need.mvdr = true;
+  rc = build_group(c, sg.g, M, 1, bins, {s}, need, nullptr, 0);
+  if (rc != GSS_OK) return rc;
+  Group& g = sg.g;
+  const size_t mb = sizeof(cdbl) * (size_t)bins * M * M;
+  CU_TRY(c, cudaMemcpyAsync(g.phi_t, tgt, mb, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.phi_b, bg, mb, cudaMemcpyHostToDevice, c->stream));
+  if (h) {
+    rc = run_mvdr_design(c, g, fixed_ref, false);
+    if (rc != GSS_OK) return rc;
+    rc = device_status(c, g);
+    if (rc != GSS_OK) return rc;
+    int z = 0;
+    CU_TRY(c, cudaMemcpyAsync(h, g.h, sizeof(cdbl) * (size_t)bins * M, cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(&z, g.zeroed, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaStreamSynchronize(c->stream));
+    if (zeroed) *zeroed = z;
+  } else {
+    MvdrArgs a;
+    a.segs = g.d_segs;
+    a.phi_t = g.phi_t;
+    a.phi_b = g.phi_b;
+    a.tmass = nullptr;
+    a.ref = g.ref;
+    a.zeroed = g.zeroed;
+    a.h = g.h;
+    a.hconj = g.hconj;
+    a.status = g.status;
+    a.M = M;
+    a.F = bins;
+    a.fixed_ref = -1;
+    CU_TRY(c, launch_select_reference(a, 1, c->stream));
+    ++c->launches;
+    int r = 0;
+    CU_TRY(c, cudaMemcpyAsync(&r, g.ref, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaStreamSynchronize(c->stream));
+    *ref_out = r;
+  }
+  return GSS_OK;
+}
+
+gss_status gss_b200_select_reference(gss_b200_ctx* c, const double* tgt, const double* bg, int32_t bins,
+                                     int32_t M, int32_t* ref) {
+  return mvdr_common(c, tgt, bg, bins, M, -1, ref, nullptr, nullptr);
+}
+
+gss_status gss_b200_mvdr(gss_b200_ctx* c, const double* tgt, const double* bg, int32_t bins, int32_t M,
+                         int32_t ref, double* h, int64_t* zeroed) {
+  if (ref < 0 || ref >= M) return fail(c, GSS_SHAPE_ERROR, "mvdr: reference channel out of range");
+  return mvdr_common(c, tgt, bg, bins, M, ref, nullptr, h, zeroed);
+}
+
+gss_status gss_b200_apply(gss_b200_ctx* c, const double* h, int32_t h_bins, int32_t h_channels, const float* y,
+                          int32_t bins, int64_t T, int32_t M, float* out) {
+  gss_status rc = check_tensor(c, bins, T, M);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  if (h_channels != M || h_bins != bins) return fail(c, GSS_SHAPE_ERROR, "beamform.apply: filter does not match tensor");
+  StageGroup sg(c);
+  SegSpec s;
+  s.T = (int)T;
+  Needs need;
+  need.y = need.x = need.mvdr = true;
+  rc = build_group(c, sg.g, M, 1, bins, {s}, need, nullptr, 0);
+  if (rc != GSS_OK) return rc;
+  Group& g = sg.g;
+  std::vector<float2> hc((size_t)bins * M);
+  for (size_t i = 0; i < hc.size(); ++i) hc[i] = make_float2((float)h[2 * i], -(float)h[2 * i + 1]);
+  CU_TRY(c, cudaMemcpyAsync(g.Y, y, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.hconj, hc.data(), sizeof(float2) * hc.size(), cudaMemcpyHostToDevice, c->stream));
+  ApplyArgs aa;
+  aa.y = g.Y;
+  aa.hconj = g.hconj;
+  aa.x = g.X;
+  aa.segs = g.d_segs;
+  aa.M = M;
+  aa.F = bins;
+  aa.frame_major = 0;
+  CU_TRY(c, launch_apply(aa, 1, (int)T, c->stream));
+  ++c->launches;
+  CU_TRY(c, cudaMemcpyAsync(out, g.X, sizeof(float2) * (size_t)bins * T, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return GSS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// beamform_kernels.cu -- reference-channel selection and Souden MVDR design
+// (beamform.hpp:89-107, :111-135), the stand-alone unit-normalisation stage
+// (wpe.hpp:124-140) and the per-sweep log-likelihood reduction
+// (cacgmm.hpp:303-305). All FP64, tiny, fixed summation order.
+#include <math_constants.h>
+
+#include "kernels.h"
+
+namespace gssb {
+
+// One warp per segment: lane c sums the diagonal entry c of the target and
+// background covariances over the bins in ascending order (the reference's
+// order), lane 0 takes the arg-max with strict '>' so ties go to the lowest
+// index. Also raises DegenerateStatsError when the target mass is not
+// positive (beamform.hpp:79-83).
+__global__ void select_reference_kernel(MvdrArgs a) {
+  const SegDev sd = a.segs[blockIdx.x];
+  const int lane = threadIdx.x;
+  const int M = a.M;
+  double num = 0.0, den = 0.0;
+  if (lane < M) {
+    for (int f = 0; f < a.F; ++f) {
+      const long long o = (sd.f_off + f) * (long long)(M * M) + lane * M + lane;
+      num += a.phi_t[o].re;
+      den += a.phi_b[o].re;
+    }
+  }
+  const double snr = lane < M ? num / fmax(den, 1e-10) : -CUDART_INF;
+  int best = 0;
+  double best_snr = -CUDART_INF;
+  for (int c = 0; c < M; ++c) {
+    const double s = __shfl_sync(0xffffffffu, snr, c);
+    if (s > best_snr) {
+      best_snr = s;
+      best = c;
+    }
+  }
+  if (lane == 0) {
+    a.ref[blockIdx.x] = a.fixed_ref >= 0 ? a.fixed_ref : best;
+    if (a.tmass != nullptr) {
+      double total = 0.0;
+      for (int f = 0; f < a.F; ++f) total += a.tmass[sd.f_off + f];
+      if (total <= 0.0) atomicMin(a.status + blockIdx.x, make_status(8 /*DegenerateStatsError*/, 0));
+    }
+  }
+}
+
+// One thread per (segment, bin): C = reg(herm(Phi_bg))^-1 Phi_target;
+// h = C[:,ref] / tr(C), zero when |tr| < 1e-10 (beamform.hpp:122-132).
+template <int M>
+__global__ void mvdr_solve_kernel(MvdrArgs a) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= a.F) return;
+  const int seg = blockIdx.y;
+  const SegDev sd = a.segs[seg];
+  const int ref = a.ref[seg];
+  const long long o = (sd.f_off + f) * (long long)(M * M);
+  cdbl A[M * M], B[M * M], work[M * M], work2[M * M];
+  double wv[M];
+  for (int i = 0; i < M * M; ++i) {
+    A[i] = a.phi_b[o + i];
+    B[i] = a.phi_t[o + i];
+  }
+  hermitize_inplace(A, M, M);
+  regularize_inplace(A, M, M, kRegEps);
+  const int st = hermitian_solve(A, M, B, M, work, work2, wv);
+  cdbl* h = a.h + (sd.f_off + f) * (long long)M;
+  float2* hc = a.hconj + (sd.f_off + f) * (long long)M;
+  if (st != kLinOk) {
+    atomicMin(a.status + seg, make_status(5 /*SingularMatrixError*/, f));
+    for (int i = 0; i < M; ++i) {
+      h[i] = cd_make(0.0, 0.0);
+      hc[i] = make_float2(0.f, 0.f);
+    }
+    return;
+  }
+  cdbl tr = cd_make(0.0, 0.0);
+  for (int i = 0; i < M; ++i) tr = cd_add(tr, B[i * M + i]);
+  if (hypot(tr.re, tr.im) < 1e-10) {
+    atomicAdd(a.zeroed + seg, 1);
+    for (int i = 0; i < M; ++i) {
+      h[i] = cd_make(0.0, 0.0);
+      hc[i] = make_float2(0.f, 0.f);
+    }
+    return;
+  }
+  for (int i = 0; i < M; ++i) {
+    const cdbl v = cd_div(B[i * M + ref], tr);
+    h[i] = v;
+    hc[i] = make_float2((float)v.re, (float)(-v.im));  // conj(h) as cfloat (beamform.hpp:159-160)
+  }
+}
+
+// y / (|y| + 1e-10) per frame, norm in double, scale in float (wpe.hpp:124-140).
+__global__ void unit_normalize_kernel(const float2* in, float2* out, long long frames, int M) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= frames) return;
+  const float2* p = in + i * M;
+  double ns = 0.0;
+  for (int c = 0; c < M; ++c) ns += (double)p[c].x * (double)p[c].x + (double)p[c].y * (double)p[c].y;
+  const float scale = (float)(1.0 / (sqrt(ns) + 1e-10));
+  for (int c = 0; c < M; ++c) out[i * M + c] = make_float2(p[c].x * scale, p[c].y * scale);
+}
+
+// ll[segment] = sum over bins in ascending order (cacgmm.hpp:303-305)
+__global__ void sum_ll_kernel(const double* bin_ll, double* out, const SegDev* segs, int nseg, int F) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const SegDev sd = segs[s];
+  double ll = 0.0;
+  for (int f = 0; f < F; ++f) ll += bin_ll[sd.f_off + f];
+  out[s] = ll;
+}
+
+cudaError_t launch_select_reference(const MvdrArgs& a, int nseg, cudaStream_t st) {
+  select_reference_kernel<<<nseg, 32, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mvdr_solve(const MvdrArgs& a, int nseg, cudaStream_t st) {
+  dim3 grid((a.F + 63) / 64, nseg);
+  switch (a.M) {
+    case 1: mvdr_solve_kernel<1><<<grid, 64, 0, st>>>(a); break;
+    case 2: mvdr_solve_kernel<2><<<grid, 64, 0, st>>>(a); break;
+    case 3: mvdr_solve_kernel<3><<<grid, 64, 0, st>>>(a); break;
+    case 4: mvdr_solve_kernel<4><<<grid, 64, 0, st>>>(a); break;
+    case 5: mvdr_solve_kernel<5><<<grid, 64, 0, st>>>(a); break;
+    case 6: mvdr_solve_kernel<6><<<grid, 64, 0, st>>>(a); break;
+    case 7: mvdr_solve_kernel<7><<<grid, 64, 0, st>>>(a); break;
+    case 8: mvdr_solve_kernel<8><<<grid, 64, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unit_normalize(const float2* in, float2* out, long long frames_total, int M, cudaStream_t st) {
+  if (frames_total == 0) return cudaSuccess;
+  unit_normalize_kernel<<<(unsigned)((frames_total + 255) / 256), 256, 0, st>>>(in, out, frames_total, M);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_ll(const double* bin_ll, double* out, const SegDev* segs, int nseg, int F, cudaStream_t st) {
+  sum_ll_kernel<<<(nseg + 63) / 64, 64, 0, st>>>(bin_ll, out, segs, nseg, F);
+  return cudaGetLastError();
+}
+
+}  // namespace gssb

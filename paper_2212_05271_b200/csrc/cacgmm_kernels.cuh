@@ -1,0 +1,569 @@
+// cacgmm_kernels.cuh -- cACGMM EM kernels (templates; instantiated per channel
+// count in cacgmm_m*.cu) and the MVDR statistics kernels that share the same
+// Hermitian outer-product machinery.
+//
+// Reference semantics: cacgmm.hpp:264-340 (em_fit), :124-152 (invert_shapes),
+// :156-174 (quad_forms), :189-257 (estep_bin), wpe.hpp:124-140 (unit_normalize),
+// numerics.hpp:128-152 (weighted_gram), beamform.hpp:35-85 (accumulate_stats).
+//
+// One EM iteration = em_pass_kernel (E-step + M-step accumulation fused in one
+// sweep over the spectrogram) + em_update_kernel (per-(f,k) M-step
+// finalisation in FP64: trace normalisation, regularisation, Cholesky inverse,
+// log-det, E-step constants for the next sweep).
+//
+// The sweep works on the RAW (un-normalised) spectrogram: with s = 1/(|y|+1e-10)
+// the unit-norm frame is s*y, so q = s^2 * q_raw and the M-step weight
+// gamma/q applied to (s*y)(s*y)^H equals (gamma/q * s^2) applied to y y^H. The
+// normalised tensor is therefore never materialised, and the last sweep can
+// accumulate the MVDR statistics of the raw tensor (beamform.hpp:35-85) with
+// the posteriors still in registers.
+#pragma once
+
+#include <math_constants.h>
+
+#include "kernels.h"
+
+namespace gssb {
+
+// ---------------------------------------------------------------------------
+// Per-lane view of one frame
+// ---------------------------------------------------------------------------
+template <int M, int L>
+struct FramePlan {
+  using Lay = EmLayout<M, L>;
+  static constexpr int NZ1 = Lay::NZ > 0 ? Lay::NZ : 1;
+  int offx[Lay::RPL];
+  int offz[Lay::RPL][NZ1];
+  bool lo[Lay::RPL];
+  float rowmask[Lay::RPL];
+
+  __device__ __forceinline__ void init(int g) {
+#pragma unroll
+    for (int i = 0; i < Lay::RPL; ++i) {
+      int row = g + i * L;
+      rowmask[i] = row < M ? 1.f : 0.f;
+      if (row >= M) row = 0;  // idle row: computes finite values that nobody reads
+      offx[i] = row;
+#pragma unroll
+      for (int d = 1; d <= Lay::D; ++d) offz[i][d - 1] = (row + d) % M;
+      if (Lay::HALF) offz[i][Lay::D] = (row + M / 2) % M;
+      lo[i] = row < M / 2;
+    }
+  }
+
+  /// Hermitian outer-product dofs of the frame whose M channels start at fr.
+  __device__ __forceinline__ void dofs(const float2* fr, float (&pv)[Lay::NDOF]) const {
+#pragma unroll
+    for (int i = 0; i < Lay::RPL; ++i) {
+      const float2 x = fr[offx[i]];
+      pv[i * M] = fmaf(x.x, x.x, x.y * x.y);
+#pragma unroll
+      for (int d = 1; d <= Lay::D; ++d) {
+        const float2 z = fr[offz[i][d - 1]];
+        pv[i * M + 2 * d - 1] = fmaf(x.x, z.x, x.y * z.y);
+        pv[i * M + 2 * d] = fmaf(x.y, z.x, -(x.x * z.y));
+      }
+      if (Lay::HALF) {
+        const float2 z = fr[offz[i][Lay::D]];
+        const float a1 = lo[i] ? x.x : x.y;
+        const float a2 = lo[i] ? x.y : -x.x;
+        pv[i * M + M - 1] = fmaf(a1, z.x, a2 * z.y);
+      }
+    }
+  }
+
+  /// |y|^2 of the frame from this lane's diagonal dofs (sum over the L lanes).
+  __device__ __forceinline__ float norm2(const float (&pv)[Lay::NDOF]) const {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < Lay::RPL; ++i) s = fmaf(rowmask[i], pv[i * M], s);
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+  }
+};
+
+/// Partial-sum cell written per (segment, bin, frame chunk): for every lane g
+/// its NA*NDOF accumulators followed by the KT class masses.
+template <int M, int L, int KT, int NA>
+struct PartLayout {
+  static constexpr int NDOF = EmLayout<M, L>::NDOF;
+  static constexpr int ACC = NA * NDOF;
+  static constexpr int STRIDE = ACC + KT;
+  static constexpr int CELL = L * STRIDE;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// E-step + accumulation sweep. grid = (work items, F), block = 256.
+// L lanes share a frame; each owns NDOF dofs of P = y y^H, the matching slice
+// of every class's B^-1 (registers) and of every accumulator. Frames stream
+// through a two-stage cp.async pipeline in shared memory.
+//   FINAL = false: accumulators are the KT M-step Grams (weights gamma/q).
+//   FINAL = true : accumulators are the MVDR target / background Grams.
+// ---------------------------------------------------------------------------
+template <int M, int L, int KT, bool FINAL>
+__global__ void __launch_bounds__(kEmThreads, 1) em_pass_kernel(EmPassArgs a) {
+  using Lay = EmLayout<M, L>;
+  constexpr int NA = FINAL ? 2 : KT;
+  using PL = PartLayout<M, L, KT, NA>;
+  constexpr int NDOF = Lay::NDOF;
+  constexpr int SLOTS = kEmThreads / L;
+  constexpr int TILE = kEmTileFrames;
+  constexpr int NW = kEmThreads / 32;
+  extern __shared__ float4 smem_f4[];
+  float2* slab = reinterpret_cast<float2*>(smem_f4);                 // 2 * TILE * M
+  float* s_ck = reinterpret_cast<float*>(slab + 2 * TILE * M);       // npat_max * KT
+  unsigned char* s_pat = reinterpret_cast<unsigned char*>(s_ck + a.npat_max * KT);  // 2 * TILE
+
+  const int tid = threadIdx.x;
+  const WorkItem wi = a.work[blockIdx.x];
+  const int f = blockIdx.y;
+  const SegDev sd = a.segs[wi.seg];
+  const int t0 = wi.chunk * sd.TC;
+  const int nt = min(sd.TC, sd.T - t0);
+  const int ntiles = (nt + TILE - 1) / TILE;
+  const float2* src = a.y + sd.y_off + ((long long)f * sd.T + t0) * M;
+  const unsigned char* psrc = a.pat + sd.pat_off + t0;
+
+  auto issue_tile = [&](int tile, int buf) {
+    const int n = min(TILE, nt - tile * TILE) * M;
+    const float2* s = src + (long long)tile * TILE * M;
+    float2* d = slab + buf * TILE * M;
+    for (int i = tid; i < n; i += kEmThreads) cp_async8(d + i, s + i);
+    cp_async_commit();
+  };
+
+  issue_tile(0, 0);
+  {
+    const float* cks = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
+    for (int i = tid; i < sd.npat * KT; i += kEmThreads) s_ck[i] = cks[i];
+    for (int i = tid; i < min(TILE, nt); i += kEmThreads) s_pat[i] = psrc[i];
+  }
+
+  const int g = tid % L, slot = tid / L;
+  float coef[KT][NDOF];
+  {
+    const float* cp = a.coef + sd.coef_off + ((long long)f * L + g) * (KT * NDOF);
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+#pragma unroll
+      for (int j = 0; j < NDOF; ++j) coef[k][j] = cp[k * NDOF + j];
+  }
+  float acc[NA][NDOF];
+  float mass[KT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) mass[k] = 0.f;
+#pragma unroll
+  for (int n = 0; n < NA; ++n)
+#pragma unroll
+    for (int j = 0; j < NDOF; ++j) acc[n][j] = 0.f;
+  double ll = 0.0;
+  FramePlan<M, L> plan;
+  plan.init(g);
+  float* gout = a.gamma != nullptr && sd.g_off >= 0
+                    ? a.gamma + sd.g_off + ((long long)f * sd.T + t0) * sd.K
+                    : nullptr;
+  const int target = sd.target;
+  const bool normalize = a.normalize != 0;
+
+  for (int tile = 0; tile < ntiles; ++tile) {
+    const int buf = tile & 1;
+    // prefetch the next tile (data by cp.async, pattern ids through registers)
+    unsigned char pnext[TILE / kEmThreads];
+    const bool more = tile + 1 < ntiles;
+    if (more) {
+      issue_tile(tile + 1, buf ^ 1);
+      const int nn = min(TILE, nt - (tile + 1) * TILE);
+#pragma unroll
+      for (int i = 0; i < TILE / kEmThreads; ++i) {
+        const int idx = tid + i * kEmThreads;
+        pnext[i] = idx < nn ? psrc[(tile + 1) * TILE + idx] : (unsigned char)0;
+      }
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int nin = min(TILE, nt - tile * TILE);
+    const float2* sl = slab + buf * TILE * M;
+    const unsigned char* sp = s_pat + buf * TILE;
+#pragma unroll 1
+    for (int fb = slot; fb < TILE; fb += SLOTS) {
+      if (fb - slot >= nin) break;  // whole stripe of slots is past the data (block-uniform per warp row)
+      const bool valid = fb < nin;
+      const int fbc = valid ? fb : nin - 1;
+      float pv[NDOF];
+      plan.dofs(sl + fbc * M, pv);
+      float inv2 = 1.f;
+      if (normalize) {
+        const float nr = __fsqrt_rn(plan.norm2(pv)) + 1e-10f;  // wpe.hpp:135
+        const float inv = __frcp_rn(nr);
+        inv2 = inv * inv;
+      }
+      float q[KT];
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < NDOF; ++j) s = fmaf(coef[k][j], pv[j], s);
+        q[k] = s;
+      }
+#pragma unroll
+      for (int o = 1; o < L; o <<= 1)
+#pragma unroll
+        for (int k = 0; k < KT; ++k) q[k] += __shfl_xor_sync(0xffffffffu, q[k], o);
+
+      const float* ckp = s_ck + (int)sp[fbc] * KT;
+      float u[KT];
+      float mx = -CUDART_INF_F;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        q[k] = fmaxf(q[k] * inv2, kQuadFloor);               // cacgmm.hpp:170-171
+        u[k] = fmaf(-(float)M, __logf(q[k]), ckp[k]);         // inactive classes carry ck = -inf
+        mx = fmaxf(mx, u[k]);
+      }
+      float se = 0.f;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        u[k] = __expf(u[k] - mx);
+        se += u[k];
+      }
+      const float rinv = valid ? __frcp_rn(se) : 0.f;
+      if (valid && g == 0) ll += (double)(mx + __logf(se));
+      float gam[KT];
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        gam[k] = u[k] * rinv;  // exactly 0 for inactive classes
+        mass[k] += gam[k];
+        if (gout != nullptr && valid && (k % L) == g && k < sd.K)
+          gout[(long long)(tile * TILE + fb) * sd.K + k] = gam[k];
+      }
+      if (FINAL) {
+        float wt = 0.f, wb = 0.f;
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          wt += (k == target) ? gam[k] : 0.f;
+          wb += (k == target) ? 0.f : gam[k];
+        }
+#pragma unroll
+        for (int j = 0; j < NDOF; ++j) {
+          acc[0][j] = fmaf(wt, pv[j], acc[0][j]);
+          acc[NA - 1][j] = fmaf(wb, pv[j], acc[NA - 1][j]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+          const float w = gam[k] * inv2 * __frcp_rn(q[k]);  // gamma / q on the unit-norm frame
+#pragma unroll
+          for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w, pv[j], acc[k][j]);
+        }
+      }
+    }
+    __syncthreads();  // everyone is done with buffer `buf` (and with s_pat[buf])
+    if (more) {
+#pragma unroll
+      for (int i = 0; i < TILE / kEmThreads; ++i) s_pat[(buf ^ 1) * TILE + tid + i * kEmThreads] = pnext[i];
+    }
+  }
+
+  // ---- reduce: frame slots within the warp, then warps through shared memory
+  if (g != 0) ll = 0.0;
+#pragma unroll
+  for (int o = L; o < 32; o <<= 1) {
+#pragma unroll
+    for (int k = 0; k < KT; ++k) mass[k] += __shfl_xor_sync(0xffffffffu, mass[k], o);
+#pragma unroll
+    for (int n = 0; n < NA; ++n)
+#pragma unroll
+      for (int j = 0; j < NDOF; ++j) acc[n][j] += __shfl_xor_sync(0xffffffffu, acc[n][j], o);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) ll += __shfl_xor_sync(0xffffffffu, ll, o);
+  __syncthreads();  // pipeline buffers are free
+  float* red = reinterpret_cast<float*>(smem_f4);
+  double* redll = reinterpret_cast<double*>(red + NW * PL::CELL + (NW * PL::CELL & 1));
+  const int lane = tid & 31, warp = tid >> 5;
+  if (lane < L) {
+    float* r = red + (warp * L + lane) * PL::STRIDE;
+#pragma unroll
+    for (int n = 0; n < NA; ++n)
+#pragma unroll
+      for (int j = 0; j < NDOF; ++j) r[n * NDOF + j] = acc[n][j];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) r[PL::ACC + k] = mass[k];
+  }
+  if (lane == 0) redll[warp] = ll;
+  __syncthreads();
+  const long long cell = sd.cell_off + (long long)f * sd.nchunks + wi.chunk;
+  float* out = a.part + cell * a.cell_stride;
+  for (int i = tid; i < PL::CELL; i += kEmThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[w * PL::CELL + i];
+    out[i] = s;
+  }
+  if (tid == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += redll[w];
+    a.cell_ll[cell] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// M-step finalisation / state preparation. grid = (ceil(F/BPB), segments),
+// block = (KT, BPB). Thread (k, b) owns class k of bin f.
+// ---------------------------------------------------------------------------
+constexpr int kUpdateBinsPerBlock = 16;
+
+template <int M, int L, int KT>
+__global__ void em_update_kernel(EmUpdateArgs a) {
+  using Lay = EmLayout<M, L>;
+  using PL = PartLayout<M, L, KT, KT>;
+  constexpr int NDOF = Lay::NDOF;
+  __shared__ double s_pi[kUpdateBinsPerBlock][KT];
+  __shared__ double s_ld[kUpdateBinsPerBlock][KT];
+
+  const int k = threadIdx.x, b = threadIdx.y;
+  const int f = blockIdx.x * kUpdateBinsPerBlock + b;
+  const int seg = blockIdx.y;
+  const SegDev sd = a.segs[seg];
+  const bool in_bin = f < a.F;
+  const bool live = in_bin && k < sd.K;
+  const long long fk = sd.fk_off + (long long)(in_bin ? f : 0) * KT + k;
+  const long long cell0 = sd.cell_off + (long long)(in_bin ? f : 0) * sd.nchunks;
+
+  if (in_bin && k == 0 && (a.mode == kEmMstep || a.mode == kEmFinal)) {
+    double ll = 0.0;
+    for (int c = 0; c < sd.nchunks; ++c) ll += a.cell_ll[cell0 + c];
+    a.bin_ll[sd.f_off + f] = ll;
+  }
+
+  double my_pi = 0.0, my_ld = 0.0;
+  if (live && a.mode != kEmFinal) {
+    cdbl gram[M * M], inv[M * M], work[M * M], fact[M * M];
+    double wv[M];
+    bool have_b = false;      // gram holds the (new) shape matrix
+    bool need_invert = false;
+    if (a.mode == kEmInit) {
+      for (int i = 0; i < M * M; ++i) gram[i] = cd_make((i / M == i % M) ? 1.0 : 0.0, 0.0);
+      my_pi = 1.0 / (double)sd.K;
+      have_b = need_invert = true;
+    } else if (a.mode == kEmFromState) {
+      for (int i = 0; i < M * M; ++i) gram[i] = a.bstate[fk * (M * M) + i];
+      my_pi = a.pi[fk];
+      need_invert = true;
+    } else {
+      double mass = 0.0;
+      for (int c = 0; c < sd.nchunks; ++c) mass += (double)a.part[(cell0 + c) * a.cell_stride + PL::ACC + k];
+      if (mass <= 0.0) {
+        // dead class at this bin: keep its shape, floor its weight (cacgmm.hpp:319-323)
+        my_pi = kWeightFloor;
+        my_ld = a.logdet[fk];
+      } else {
+        for (int i = 0; i < M * M; ++i) gram[i] = cd_make(0.0, 0.0);
+        for (int g = 0; g < L; ++g)
+          for (int j = 0; j < NDOF; ++j) {
+            const DofInfo di = dof_info(M, L, g, j);
+            if (di.kind == kIdle) continue;
+            double v = 0.0;
+            for (int c = 0; c < sd.nchunks; ++c)
+              v += (double)a.part[(cell0 + c) * a.cell_stride + g * PL::STRIDE + k * NDOF + j];
+            dof_scatter(gram, M, di, v);
+          }
+        const double s = (double)M / mass;  // cacgmm.hpp:327-329
+        double tr = 0.0;
+        for (int i = 0; i < M * M; ++i) gram[i] = cd_scale(gram[i], s);
+        hermitize_inplace(gram, M, M);
+        for (int i = 0; i < M; ++i) tr += gram[i * M + i].re;
+        if (tr > 0.0) {
+          const double gsc = (double)M / tr;
+          for (int i = 0; i < M * M; ++i) gram[i] = cd_scale(gram[i], gsc);
+        }
+        regularize_inplace(gram, M, M, kRegEps);
+        my_pi = fmax(kWeightFloor, mass / (double)sd.T);
+        have_b = need_invert = true;
+      }
+    }
+    if (have_b)
+      for (int i = 0; i < M * M; ++i) a.bstate[fk * (M * M) + i] = gram[i];
+    if (need_invert) {
+      // invert_shapes: plain attempt, then once more on regularize(B) (cacgmm.hpp:134-140)
+      for (int i = 0; i < M * M; ++i) fact[i] = gram[i];
+      int st = hermitian_inverse_logdet<M>(fact, M, inv, &my_ld, work, wv);
+      if (st != kLinOk) {
+        for (int i = 0; i < M * M; ++i) fact[i] = gram[i];
+        regularize_inplace(fact, M, M, kRegEps);
+        st = hermitian_inverse_logdet<M>(fact, M, inv, &my_ld, work, wv);
+      }
+      if (st != kLinOk) {
+        atomicMin(&a.status[seg], make_status(5 /*SingularMatrixError*/, f));
+        my_ld = 0.0;
+        for (int i = 0; i < M * M; ++i) inv[i] = cd_make((i / M == i % M) ? 1.0 : 0.0, 0.0);
+      }
+      // B^-1 is rounded to cfloat before use (cacgmm.hpp:144-149)
+      for (int g = 0; g < L; ++g) {
+        float* cp = a.coef + sd.coef_off + ((long long)f * L + g) * (KT * NDOF) + k * NDOF;
+        for (int j = 0; j < NDOF; ++j) cp[j] = dof_coef(inv, M, dof_info(M, L, g, j));
+      }
+      a.logdet[fk] = my_ld;
+    }
+    a.pi[fk] = my_pi;
+  } else if (in_bin && (a.mode == kEmInit || a.mode == kEmFromState)) {
+    // padded class (K <= k < KT): zero coefficients; it is masked off by ck = -inf
+    for (int g = 0; g < L; ++g) {
+      float* cp = a.coef + sd.coef_off + ((long long)f * L + g) * (KT * NDOF) + k * NDOF;
+      for (int j = 0; j < NDOF; ++j) cp[j] = 0.f;
+    }
+  }
+  s_pi[b][k] = my_pi;
+  s_ld[b][k] = my_ld;
+  __syncthreads();
+  if (!in_bin || a.mode == kEmFinal) return;
+
+  // E-step constants per activity pattern (cacgmm.hpp:196-237):
+  //   ck = lp + c0 - log|B_k|, lp = log max(1e-10, pi_k) - log z, z = sum of active pi
+  const double c0 = -(double)M * log(2.0 * 3.14159265358979323846) + lgamma((double)M);
+  float* tab = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
+  for (int p = 0; p < sd.npat; ++p) {
+    const uint32_t mask = a.masks[sd.mask_off + p];
+    float v = -CUDART_INF_F;
+    if (k < sd.K) {
+      double z = 0.0;
+      for (int kk = 0; kk < sd.K; ++kk)
+        if (mask & (1u << kk)) z += s_pi[b][kk];
+      bool active;
+      double lp;
+      if (z <= 0.0) {  // no active class: noise class alone, or uniform (cacgmm.hpp:217-226)
+        active = sd.noise >= 0 ? k == sd.noise : true;
+        lp = sd.noise >= 0 ? 0.0 : -log((double)sd.K);
+      } else {
+        active = (mask >> k) & 1u;
+        lp = log(fmax(kWeightFloor, s_pi[b][k])) - log(z);
+      }
+      if (active) v = (float)(lp + c0 - s_ld[b][k]);
+    }
+    tab[p * KT + k] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MVDR statistics from posteriors held in memory (the stage entry point of
+// beamform.hpp:35-85). Same lane layout and cell format as the FINAL sweep.
+// ---------------------------------------------------------------------------
+template <int M, int L, int KT>
+__global__ void __launch_bounds__(kEmThreads) mvdr_stats_kernel(StatsPassArgs a) {
+  using Lay = EmLayout<M, L>;
+  using PL = PartLayout<M, L, KT, 2>;
+  constexpr int NDOF = Lay::NDOF;
+  constexpr int SLOTS = kEmThreads / L;
+  constexpr int NW = kEmThreads / 32;
+  extern __shared__ float4 smem_f4[];
+  float* red = reinterpret_cast<float*>(smem_f4);
+
+  const int tid = threadIdx.x;
+  const WorkItem wi = a.work[blockIdx.x];
+  const int f = blockIdx.y;
+  const SegDev sd = a.segs[wi.seg];
+  const int t0 = wi.chunk * sd.TC;
+  const int nt = min(sd.TC, sd.T - t0);
+  const int g = tid % L, slot = tid / L;
+  const float2* src = a.y + sd.y_off + ((long long)f * sd.T + t0) * M;
+  const float* gsrc = a.gamma + sd.g_off + ((long long)f * sd.T + t0) * sd.K;
+  FramePlan<M, L> plan;
+  plan.init(g);
+  float acc_t[NDOF], acc_b[NDOF];
+#pragma unroll
+  for (int j = 0; j < NDOF; ++j) acc_t[j] = acc_b[j] = 0.f;
+  float tmass = 0.f;
+  for (int fb = slot; fb < nt; fb += SLOTS) {
+    float pv[NDOF];
+    plan.dofs(src + (long long)fb * M, pv);  // straight from global/L2: one use per element
+    const float* gr = gsrc + (long long)fb * sd.K;
+    const float wt = gr[sd.target];
+    float wb = 0.f;
+    for (int k = 0; k < sd.K; ++k)
+      if (k != sd.target) wb += gr[k];
+    tmass += wt;
+#pragma unroll
+    for (int j = 0; j < NDOF; ++j) {
+      acc_t[j] = fmaf(wt, pv[j], acc_t[j]);
+      acc_b[j] = fmaf(wb, pv[j], acc_b[j]);
+    }
+  }
+#pragma unroll
+  for (int o = L; o < 32; o <<= 1) {
+#pragma unroll
+    for (int j = 0; j < NDOF; ++j) {
+      acc_t[j] += __shfl_xor_sync(0xffffffffu, acc_t[j], o);
+      acc_b[j] += __shfl_xor_sync(0xffffffffu, acc_b[j], o);
+    }
+    tmass += __shfl_xor_sync(0xffffffffu, tmass, o);
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+  if (lane < L) {
+    float* r = red + (warp * L + lane) * PL::STRIDE;
+#pragma unroll
+    for (int j = 0; j < NDOF; ++j) {
+      r[j] = acc_t[j];
+      r[NDOF + j] = acc_b[j];
+    }
+#pragma unroll
+    for (int k = 0; k < KT; ++k) r[PL::ACC + k] = (k == sd.target) ? tmass : 0.f;
+  }
+  __syncthreads();
+  float* out = a.part + (sd.cell_off + (long long)f * sd.nchunks + wi.chunk) * a.cell_stride;
+  for (int i = tid; i < PL::CELL; i += kEmThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[w * PL::CELL + i];
+    out[i] = s;
+  }
+}
+
+/// chunk partials -> Phi_target, Phi_background (x 1/T) in FP64. One thread per (seg, f).
+template <int M, int L, int KT>
+__global__ void mvdr_stats_final_kernel(StatsFinalArgs a) {
+  using PL = PartLayout<M, L, KT, 2>;
+  constexpr int NDOF = PL::NDOF;
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= a.F) return;
+  const SegDev sd = a.segs[blockIdx.y];
+  const long long cell0 = sd.cell_off + (long long)f * sd.nchunks;
+  cdbl gt[M * M], gb[M * M];
+  for (int i = 0; i < M * M; ++i) gt[i] = gb[i] = cd_make(0.0, 0.0);
+  for (int g = 0; g < L; ++g)
+    for (int j = 0; j < NDOF; ++j) {
+      const DofInfo di = dof_info(M, L, g, j);
+      if (di.kind == kIdle) continue;
+      double vt = 0.0, vb = 0.0;
+      for (int c = 0; c < sd.nchunks; ++c) {
+        const float* p = a.part + (cell0 + c) * a.cell_stride + g * PL::STRIDE;
+        vt += (double)p[j];
+        vb += (double)p[NDOF + j];
+      }
+      dof_scatter(gt, M, di, vt);
+      dof_scatter(gb, M, di, vb);
+    }
+  double mass = 0.0;
+  for (int c = 0; c < sd.nchunks; ++c) mass += (double)a.part[(cell0 + c) * a.cell_stride + PL::ACC + sd.target];
+  const double inv_t = 1.0 / (double)sd.T;
+  const long long o = (sd.f_off + f) * (long long)(M * M);
+  for (int i = 0; i < M * M; ++i) {
+    a.phi_t[o + i] = cd_scale(gt[i], inv_t);
+    a.phi_b[o + i] = cd_scale(gb[i], inv_t);
+  }
+  a.tmass[sd.f_off + f] = mass;
+}
+
+}  // namespace gssb

@@ -1,0 +1,153 @@
+// kernels.h -- argument blocks and launchers of the stage kernels (internal).
+#pragma once
+
+#include "gss_internal.cuh"
+
+namespace gssb {
+
+// ---- STFT / iSTFT / apply (stft_kernels.cu) --------------------------------
+struct StftArgs {
+  const float* audio;
+  float2* y;
+  const SegDev* segs;
+  const float2* tw;   // exp(-2 pi i k / n), k < n/2
+  const float* win;   // analysis window, n floats
+  StftParams p;
+  int M, TB;
+};
+struct ApplyArgs {
+  const float2* y;
+  const float2* hconj;  // (f, M): conj(h) rounded to cfloat
+  float2* x;            // (T, F) per segment (frame_major) or (F, T)
+  const SegDev* segs;
+  int M, F;
+  int frame_major;
+};
+struct IstftArgs {
+  const float2* x;
+  float* wave;
+  const SegDev* segs;
+  const float2* tw;
+  const float* win;
+  StftParams p;
+  int HB;
+};
+cudaError_t launch_stft(const StftArgs& a, int nseg, int max_frames, cudaStream_t st);
+cudaError_t launch_apply(const ApplyArgs& a, int nseg, int max_frames, cudaStream_t st);
+cudaError_t launch_istft(const IstftArgs& a, int nseg, long long max_out_len, cudaStream_t st);
+
+// ---- WPE (wpe_kernels.cu) ---------------------------------------------------
+struct WpeArgs {
+  const float2* yobs;   // observed spectrogram
+  const float2* ycur;   // current estimate (power source)
+  float2* yout;         // next estimate
+  float* w;             // (F,T) weights
+  float2* gram;         // tiles
+  float2* gconj;        // (F, km, M)
+  const SegDev* segs;
+  status_t* status;
+  double regularization;
+  int M, taps, delay, psd_context;
+};
+int wpe_gram_tiles(int km);
+/// power -> gram -> solve -> apply (4 launches)
+cudaError_t launch_wpe_iteration(const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
+                                 cudaStream_t st, long long* launches);
+
+// ---- cACGMM EM + MVDR statistics (cacgmm_kernels.cuh, cacgmm_m*.cu) -----------
+enum EmUpdateMode { kEmInit = 0, kEmMstep = 1, kEmFinal = 2, kEmFromState = 3 };
+
+struct EmPassArgs {
+  const float2* y;
+  const SegDev* segs;
+  const WorkItem* work;
+  const unsigned char* pat;
+  const float* ck;
+  const float* coef;
+  float* part;
+  double* cell_ll;
+  float* gamma;       // nullable: posteriors of this sweep
+  int cell_stride;    // floats per partial cell
+  int npat_max;
+  int normalize;      // 1: frames are unit-normalised on the fly (wpe.hpp:124-140)
+};
+struct EmUpdateArgs {
+  const SegDev* segs;
+  const uint32_t* masks;
+  const float* part;
+  const double* cell_ll;
+  cdbl* bstate;     // (fk, M*M) shape matrices B
+  double* pi;       // (fk)
+  double* logdet;   // (fk)
+  float* coef;
+  float* ck;
+  double* bin_ll;   // (f) slot of this sweep
+  status_t* status; // per segment of the group
+  int cell_stride;
+  int mode;
+  int F;
+};
+struct StatsPassArgs {
+  const float2* y;
+  const float* gamma;
+  const SegDev* segs;
+  const WorkItem* work;
+  float* part;
+  int cell_stride;
+};
+struct StatsFinalArgs {
+  const SegDev* segs;
+  const float* part;
+  cdbl* phi_t;     // (f, M*M)
+  cdbl* phi_b;     // (f, M*M)
+  double* tmass;   // (f)
+  int cell_stride;
+  int F;
+};
+
+/// Lanes cooperating on one frame, chosen so the per-thread register tiles
+/// (2 * KT * NDOF floats) stay in registers.
+constexpr int em_lanes(int M, int KT) {
+  if (M == 1) return 1;
+  if (M <= 4) return 2;
+  if (M == 5) return KT <= 5 ? 2 : 4;
+  if (M == 6) return 4;
+  if (M == 7) return KT <= 6 ? 4 : 8;
+  return KT <= 5 ? 4 : 8;
+}
+/// Class count the kernels are instantiated for (>= K).
+constexpr int em_class_tier(int K) { return K <= 2 ? 2 : K <= 3 ? 3 : K <= 4 ? 4 : K <= 5 ? 5 : K <= 6 ? 6 : 8; }
+constexpr int em_ndof(int M, int L) { return ((M + L - 1) / L) * M; }
+/// floats per partial cell (covers both sweep flavours)
+constexpr int em_cell_floats(int M, int KT) {
+  return em_lanes(M, KT) * ((KT > 2 ? KT : 2) * em_ndof(M, em_lanes(M, KT)) + KT);
+}
+
+struct EmShape {
+  int M, KT;
+};
+cudaError_t launch_em_pass(EmShape s, bool final_sweep, const EmPassArgs& a, int nwork, int F, cudaStream_t st);
+cudaError_t launch_em_update(EmShape s, const EmUpdateArgs& a, int nseg, cudaStream_t st);
+cudaError_t launch_mvdr_stats(EmShape s, const StatsPassArgs& a, int nwork, int F, cudaStream_t st);
+cudaError_t launch_mvdr_stats_final(EmShape s, const StatsFinalArgs& a, int nseg, cudaStream_t st);
+
+// ---- beamformer design + misc (beamform_kernels.cu) -------------------------------
+struct MvdrArgs {
+  const SegDev* segs;
+  const cdbl* phi_t;
+  const cdbl* phi_b;
+  const double* tmass;
+  int* ref;            // per segment (in/out)
+  int* zeroed;         // per segment
+  cdbl* h;             // (f, M)
+  float2* hconj;       // (f, M)
+  status_t* status;
+  int M, F;
+  int fixed_ref;       // >= 0: use this reference channel instead of selecting
+};
+cudaError_t launch_select_reference(const MvdrArgs& a, int nseg, cudaStream_t st);
+cudaError_t launch_mvdr_solve(const MvdrArgs& a, int nseg, cudaStream_t st);
+cudaError_t launch_unit_normalize(const float2* in, float2* out, long long frames_total, int M, cudaStream_t st);
+cudaError_t launch_sum_ll(const double* bin_ll, double* out, const SegDev* segs, int nseg, int F, cudaStream_t st);
+
+}  // namespace gssb

@@ -1,0 +1,260 @@
+// stft_kernels.cu -- batched STFT analysis, beamformer application and fused
+// inverse STFT / overlap-add.
+//
+// Reference semantics: stft.hpp:100-116 (reflect padding without edge repeat),
+// :120-129 (frame geometry), :131-175 (analyze), :179-229 (synthesize),
+// beamform.hpp:138-165 (apply).
+//
+// FFTs: one warp transforms one complex sequence of n points in shared memory
+// (radix-2 decimation in time). Two real sequences ride in one complex
+// transform (x1 + i x2), which halves the work of the real transforms.
+#include "kernels.h"
+
+namespace gssb {
+
+namespace {
+
+constexpr int kStftThreads = 256;
+constexpr int kStftWarps = kStftThreads / 32;
+
+/// In-place radix-2 DIT over bit-reversed input; tw[k] = exp(-2 pi i k / n).
+/// INVERSE conjugates the twiddles (unscaled inverse).
+template <bool INVERSE>
+__device__ __forceinline__ void warp_fft(float2* buf, const float2* __restrict__ tw, int n, int log2n,
+                                         int lane) {
+  for (int s = 1; s <= log2n; ++s) {
+    const int half = 1 << (s - 1);
+    const int tstep = n >> s;
+    for (int b = lane; b < (n >> 1); b += 32) {
+      const int pos = b & (half - 1);
+      const int i0 = ((b >> (s - 1)) << s) + pos;
+      const int i1 = i0 + half;
+      float2 w = tw[pos * tstep];
+      if (INVERSE) w.y = -w.y;
+      const float2 u = buf[i0], x = buf[i1];
+      const float2 v = make_float2(x.x * w.x - x.y * w.y, x.x * w.y + x.y * w.x);
+      buf[i0] = make_float2(u.x + v.x, u.y + v.y);
+      buf[i1] = make_float2(u.x - v.x, u.y - v.y);
+    }
+    __syncwarp();
+  }
+}
+
+/// Source index of padded position p (stft.hpp:100-116); N >= 2.
+__device__ __forceinline__ long long reflect_index(long long idx, long long N) {
+  if (idx < 0) return -idx;  // left pad: out[i] = x[pad - i]
+  if (idx >= N) {
+    long long src = N - 2 - (idx - N);
+    while (src < 0 || src >= N) {
+      if (src < 0) src = -src;
+      if (src >= N) src = 2 * (N - 1) - src;
+    }
+    return src;
+  }
+  return idx;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// analyze: grid (frame tiles, segments). A CTA transforms TB frames of all M
+// channels, assembles the (f, frame, channel) tile in shared memory and writes
+// runs of TB*M contiguous cfloats per bin (the (F,T,M) layout of stft.hpp:52-80).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kStftThreads) stft_kernel(StftArgs a) {
+  extern __shared__ float4 smem_f4[];
+  float2* fftbuf = reinterpret_cast<float2*>(smem_f4);
+  const int n = a.p.fft_size, log2n = a.p.log2n, F = a.p.F, M = a.M, TB = a.TB;
+  float2* tile = fftbuf + kStftWarps * n;
+  const int run = TB * M;
+  const int pitch = run | 1;
+  const SegDev sd = a.segs[blockIdx.y];
+  const int t0 = blockIdx.x * TB;
+  if (t0 >= sd.T) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pad = n / 2;
+  const long long N = sd.N;
+  float2* buf = fftbuf + warp * n;
+  const int npairs = (run + 1) / 2;
+  for (int pair = warp; pair < npairs; pair += kStftWarps) {
+    const int s1 = 2 * pair, s2 = s1 + 1;
+    const int tl1 = s1 / M, m1 = s1 % M, tl2 = s2 / M, m2 = s2 % M;
+    const bool v1 = t0 + tl1 < sd.T;
+    const bool v2 = s2 < run && t0 + tl2 < sd.T;
+    const float* x1 = a.audio + sd.audio_off + (long long)m1 * N;
+    const float* x2 = a.audio + sd.audio_off + (long long)m2 * N;
+    const long long b1 = (long long)(t0 + tl1) * a.p.shift - pad;
+    const long long b2 = (long long)(t0 + tl2) * a.p.shift - pad;
+    for (int i = lane; i < n; i += 32) {
+      const float w = a.win[i];
+      const float r1 = v1 ? x1[reflect_index(b1 + i, N)] * w : 0.f;
+      const float r2 = v2 ? x2[reflect_index(b2 + i, N)] * w : 0.f;
+      buf[__brev((unsigned)i) >> (32 - log2n)] = make_float2(r1, r2);
+    }
+    __syncwarp();
+    warp_fft<false>(buf, a.tw, n, log2n, lane);
+    for (int f = lane; f <= n / 2; f += 32) {
+      const float2 zf = buf[f], zn = buf[(n - f) & (n - 1)];
+      if (v1) tile[f * pitch + s1] = make_float2(0.5f * (zf.x + zn.x), 0.5f * (zf.y - zn.y));
+      if (v2) tile[f * pitch + s2] = make_float2(0.5f * (zf.y + zn.y), 0.5f * (zn.x - zf.x));
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  const int nvalid = min(TB, sd.T - t0) * M;
+  float2* out = a.y + sd.y_off + (long long)t0 * M;
+  for (int e = threadIdx.x; e < F * nvalid; e += kStftThreads) {
+    const int f = e / nvalid, r = e - f * nvalid;
+    out[(long long)f * sd.T * M + r] = tile[f * pitch + r];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// apply: X(t,f) = sum_c y(f,t,c) * conj(h(f,c)) (beamform.hpp:157-163), written
+// frame-major so the inverse transform reads each frame's bins contiguously.
+// grid (frame tiles of 32, bin tiles of 32, segments), block 32 x 8.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) beamform_apply_kernel(ApplyArgs a) {
+  __shared__ float2 tile[32][33];
+  const SegDev sd = a.segs[blockIdx.z];
+  const int t0 = blockIdx.x * 32, f0 = blockIdx.y * 32;
+  if (t0 >= sd.T) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int M = a.M, F = a.F;
+  const int t = t0 + tx;
+  for (int fy = ty; fy < 32; fy += 8) {
+    const int f = f0 + fy;
+    float2 s = make_float2(0.f, 0.f);
+    if (f < F && t < sd.T) {
+      const float2* y = a.y + sd.y_off + ((long long)f * sd.T + t) * M;
+      const float2* hc = a.hconj + (sd.f_off + f) * (long long)M;
+      for (int c = 0; c < M; ++c) {
+        const float2 v = y[c], h = hc[c];
+        // complex<float> multiply-accumulate, as Eigen's cfloat GEMV does
+        s.x += v.x * h.x - v.y * h.y;
+        s.y += v.x * h.y + v.y * h.x;
+      }
+    }
+    tile[fy][tx] = s;
+    if (!a.frame_major && f < F && t < sd.T) a.x[sd.x_off + (long long)f * sd.T + t] = s;
+  }
+  if (!a.frame_major) return;
+  __syncthreads();
+  for (int ty2 = ty; ty2 < 32; ty2 += 8) {
+    const int tt = t0 + ty2, f = f0 + tx;
+    if (tt < sd.T && f < F) a.x[sd.x_off + (long long)tt * F + f] = tile[tx][ty2];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// synthesize: inverse real FFT (scaled 1/n), window, overlap-add, divide by the
+// window-power sum, trim the padding (stft.hpp:196-227). grid (hop blocks,
+// segments); a CTA produces HB hops of output and transforms the HB+R-1 frames
+// that overlap them, so the overlap-add is a gather (no atomics, fixed order).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kStftThreads) istft_kernel(IstftArgs a) {
+  extern __shared__ float4 smem_f4[];
+  float2* fftbuf = reinterpret_cast<float2*>(smem_f4);
+  const int n = a.p.fft_size, log2n = a.p.log2n, F = a.p.F, shift = a.p.shift, HB = a.HB;
+  float* frames = reinterpret_cast<float*>(fftbuf + kStftWarps * n);
+  const SegDev sd = a.segs[blockIdx.y];
+  const long long out_len = sd.N;
+  const int pad = n / 2, R = n / shift;
+  const long long p_lo = (long long)pad + (long long)blockIdx.x * HB * shift;
+  if (p_lo - pad >= out_len) return;
+  const long long h_lo = p_lo / shift;
+  const long long t_first = h_lo - R + 1;
+  const int NF = HB + R - 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float2* buf = fftbuf + warp * n;
+  const float inv_n = 1.0f / (float)n;
+  const float2* X = a.x + sd.x_off;
+  for (int pair = warp; pair < (NF + 1) / 2; pair += kStftWarps) {
+    const int la = 2 * pair, lb = la + 1;
+    const long long ta = t_first + la, tb = t_first + lb;
+    const bool va = ta >= 0 && ta < sd.T;
+    const bool vb = lb < NF && tb >= 0 && tb < sd.T;
+    if (va || vb) {
+      for (int k = lane; k <= n / 2; k += 32) {
+        const float2 xa = va ? X[ta * F + k] : make_float2(0.f, 0.f);
+        const float2 xb = vb ? X[tb * F + k] : make_float2(0.f, 0.f);
+        if (k == 0 || k == n / 2) {
+          // imaginary parts of DC / Nyquist are ignored by the real inverse
+          buf[__brev((unsigned)k) >> (32 - log2n)] = make_float2(xa.x, xb.x);
+        } else {
+          buf[__brev((unsigned)k) >> (32 - log2n)] = make_float2(xa.x - xb.y, xa.y + xb.x);
+          buf[__brev((unsigned)(n - k)) >> (32 - log2n)] = make_float2(xa.x + xb.y, xb.x - xa.y);
+        }
+      }
+      __syncwarp();
+      warp_fft<true>(buf, a.tw, n, log2n, lane);
+    }
+    for (int i = lane; i < n; i += 32) {
+      const float w = a.win[i] * inv_n;
+      const float2 z = (va || vb) ? buf[i] : make_float2(0.f, 0.f);
+      frames[la * n + i] = va ? z.x * w : 0.f;
+      if (lb < NF) frames[lb * n + i] = vb ? z.y * w : 0.f;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  float* out = a.wave + sd.wave_off;
+  for (int j = threadIdx.x; j < HB * shift; j += kStftThreads) {
+    const long long p = p_lo + j;
+    const long long i = p - pad;
+    if (i >= out_len) break;
+    const long long h = p / shift;
+    float acc = 0.f, ws = 0.f;
+    for (int r = R - 1; r >= 0; --r) {  // ascending frame index, as the reference adds them
+      const long long t = h - r;
+      if (t < 0 || t >= sd.T) continue;
+      const int off = (int)(p - t * shift);
+      const float w = a.win[off];
+      acc += frames[(int)(t - t_first) * n + off];
+      ws = fmaf(w, w, ws);
+    }
+    out[i] = ws > 1e-8f ? acc / ws : 0.f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static int stft_frames_per_cta(int n) { return n >= 4096 ? 1 : 4096 / n; }
+
+cudaError_t launch_stft(const StftArgs& args_in, int nseg, int max_frames, cudaStream_t st) {
+  StftArgs a = args_in;
+  a.TB = stft_frames_per_cta(a.p.fft_size);
+  const size_t smem =
+      sizeof(float2) * ((size_t)kStftWarps * a.p.fft_size + (size_t)a.p.F * ((a.TB * a.M) | 1));
+  if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(stft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((max_frames + a.TB - 1) / a.TB, nseg);
+  stft_kernel<<<grid, kStftThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply(const ApplyArgs& a, int nseg, int max_frames, cudaStream_t st) {
+  dim3 grid((max_frames + 31) / 32, (a.F + 31) / 32, nseg);
+  beamform_apply_kernel<<<grid, dim3(32, 8), 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_istft(const IstftArgs& args_in, int nseg, long long max_out_len, cudaStream_t st) {
+  IstftArgs a = args_in;
+  a.HB = 16;
+  const int R = a.p.fft_size / a.p.shift;
+  const size_t smem = sizeof(float2) * (size_t)kStftWarps * a.p.fft_size +
+                      sizeof(float) * (size_t)(a.HB + R - 1) * a.p.fft_size;
+  if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(istft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long per = (long long)a.HB * a.p.shift;
+  dim3 grid((unsigned)((max_out_len + per - 1) / per), nseg);
+  if (grid.x == 0) return cudaSuccess;
+  istft_kernel<<<grid, kStftThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace gssb

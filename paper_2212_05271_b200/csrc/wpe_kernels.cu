@@ -1,0 +1,427 @@
+// wpe_kernels.cu -- WPE dereverberation (wpe.hpp:40-56 frame powers, :61-98
+// per-bin iteration, :105-120 driver; numerics.hpp:81-94 Hermitian solve,
+// :128-152 weighted Gram).
+//
+// Window formulation. The reference materialises, per frame t, the tap-stacked
+// row a_t = [y_{t-d}, y_{t-d-1}, ..., y_{t-d-taps+1} | y_t]. With the taps
+// stored in REVERSE order the stacked history is one contiguous slice of the
+// per-bin slab: element e = u*M + c (u = taps-1-k) of the history of frame t is
+// y[t - H + u][c], H = d + taps - 1. So the correlation matrix
+//   R[e][e'] = sum_t w_t y[t-H+e/M][e%M] conj(y[t-H+e'/M][e'%M])
+// and the cross term P[e][c] = sum_t w_t y[t-H+e/M][e%M] conj(y[t][c]) are
+// windowed correlations of the slab with itself; the tap-stacked matrix is
+// never built. The solve runs in the same (permuted) ordering; a symmetric
+// permutation of R leaves G = R^-1 P unchanged up to rounding order.
+//
+// Kernels per iteration:
+//   wpe_power_kernel  w_t = 1/lambda_t from the current estimate
+//   wpe_gram_kernel   8x8 complex register tiles, one warp per tile, one lane
+//                     per frame; slab staged channel-major in shared memory
+//   wpe_solve_kernel  FP64 Cholesky of the km x km system per (segment, bin)
+//   wpe_apply_kernel  Y_f = observed - history * conj(G)
+#include "kernels.h"
+
+namespace gssb {
+
+namespace {
+
+constexpr int kGramWarps = 8;
+constexpr int kGramThreads = kGramWarps * 32;
+constexpr int kGramTileFrames = 512;  // frames staged per shared-memory tile
+
+__host__ __device__ inline int gram_row_blocks(int km) { return (km + 7) / 8; }
+__host__ __device__ inline int gram_num_tiles(int km) {
+  const int nb = gram_row_blocks(km);
+  return nb * (nb + 1) / 2 + nb;
+}
+
+/// tile index -> (row block, column block); column block == nb marks the
+/// cross-term tile against the current frame.
+__device__ __forceinline__ void gram_tile_coords(int tile, int nb, int& bi, int& bj) {
+  const int ntri = nb * (nb + 1) / 2;
+  if (tile >= ntri) {
+    bi = tile - ntri;
+    bj = nb;
+    return;
+  }
+  int r = 0;
+  while ((r + 1) * (r + 2) / 2 <= tile) ++r;
+  bi = r;
+  bj = tile - r * (r + 1) / 2;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// lambda_t and the Gram weights (wpe.hpp:40-56, :86-87). One thread per (f,t).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) wpe_power_kernel(WpeArgs a) {
+  const SegDev sd = a.segs[blockIdx.z];
+  if (!sd.wpe_active) return;
+  const int f = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sd.T) return;
+  const int M = a.M;
+  const float2* y = a.ycur + sd.y_off + (long long)f * sd.T * M;
+  const int lo = max(0, t - a.psd_context), hi = min(sd.T - 1, t + a.psd_context);
+  double acc = 0.0;
+  for (int u = lo; u <= hi; ++u) {
+    float s = 0.f;  // Eigen's squaredNorm on a cfloat row accumulates in float
+    for (int c = 0; c < M; ++c) {
+      const float2 v = y[(long long)u * M + c];
+      s += v.x * v.x + v.y * v.y;
+    }
+    acc += (double)s / (double)M;
+  }
+  const float lambda = (float)fmax(kPowerFloor, acc / (double)(hi - lo + 1));
+  a.w[sd.w_off + (long long)f * sd.T + t] = 1.0f / lambda;
+}
+
+// ---------------------------------------------------------------------------
+// Weighted Gram. grid (tile groups * wchunks, F, segments), block 256.
+// Warp w of group g owns output tile g*8+w for the CTA's whole frame range;
+// lane l accumulates frames l, l+32, ... and the 32 lanes are summed at the end.
+// Shared slab: [channel][frame] (pitch odd) so a warp's loads are contiguous.
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
+  extern __shared__ float4 smem_f4[];
+  const SegDev sd = a.segs[blockIdx.z];
+  if (!sd.wpe_active) return;
+  const int f = blockIdx.y;
+  const int km = a.taps * M, nb = gram_row_blocks(km), ntiles = gram_num_tiles(km);
+  const int ngroups = (ntiles + kGramWarps - 1) / kGramWarps;
+  const int group = blockIdx.x % ngroups, chunk = blockIdx.x / ngroups;
+  if (chunk >= sd.wchunks) return;
+  const int H = a.delay + a.taps - 1;
+  const int SF = kGramTileFrames + H;      // slab frames per tile (history halo first)
+  const int pitch = SF | 1;
+  float2* slab = reinterpret_cast<float2*>(smem_f4);          // M * pitch
+  float* wsm = reinterpret_cast<float*>(slab + M * pitch);     // kGramTileFrames
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = group * kGramWarps + warp;
+  const bool live = tile < ntiles;
+  int bi = 0, bj = 0;
+  if (live) gram_tile_coords(tile, nb, bi, bj);
+  int rowoff[8], coloff[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    // rows / columns past km (padding of the last block) alias the last valid
+    // element; their outputs are never read
+    const int e = min(8 * bi + r, km - 1);
+    rowoff[r] = (e % M) * pitch + e / M;
+    if (bj == nb) {
+      coloff[r] = (r < M ? r : 0) * pitch + H;
+    } else {
+      const int e2 = min(8 * bj + r, km - 1);
+      coloff[r] = (e2 % M) * pitch + e2 / M;
+    }
+  }
+  float accr[8][8], acci[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) accr[r][c] = acci[r][c] = 0.f;
+
+  const int t_begin = chunk * sd.WTC, t_end = min(sd.T, t_begin + sd.WTC);
+  const float2* yf = a.yobs + sd.y_off + (long long)f * sd.T * M;
+  const float* wf = a.w + sd.w_off + (long long)f * sd.T;
+  for (int tb = t_begin; tb < t_end; tb += kGramTileFrames) {
+    const int nfr = min(kGramTileFrames, t_end - tb);
+    __syncthreads();
+    // stage frames [tb-H, tb+nfr) channel-major; frames < 0 are zero (wpe.hpp:74-75)
+    for (int i = tid; i < (nfr + H) * M; i += kGramThreads) {
+      const int fr = i / M, c = i - fr * M;
+      const int t = tb - H + fr;
+      slab[c * pitch + fr] = t >= 0 ? yf[(long long)t * M + c] : make_float2(0.f, 0.f);
+    }
+    for (int i = tid; i < nfr; i += kGramThreads) wsm[i] = wf[tb + i];
+    __syncthreads();
+    if (live) {
+      for (int fi = lane; fi < nfr; fi += 32) {
+        const float w = wsm[fi];
+        float2 ar[8], bc[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) ar[r] = slab[rowoff[r] + fi];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float2 v = slab[coloff[c] + fi];
+          bc[c] = make_float2(v.x * w, v.y * w);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            // a * conj(b)
+            accr[r][c] = fmaf(ar[r].x, bc[c].x, accr[r][c]);
+            accr[r][c] = fmaf(ar[r].y, bc[c].y, accr[r][c]);
+            acci[r][c] = fmaf(ar[r].y, bc[c].x, acci[r][c]);
+            acci[r][c] = fmaf(-ar[r].x, bc[c].y, acci[r][c]);
+          }
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        accr[r][c] += __shfl_xor_sync(0xffffffffu, accr[r][c], o);
+        acci[r][c] += __shfl_xor_sync(0xffffffffu, acci[r][c], o);
+      }
+  float2* out = a.gram + ((sd.wcell_off + (long long)f * sd.wchunks + chunk) * ntiles + tile) * 64;
+  // lane l writes entries l and l+32 (static register indices: select by predicate)
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int idx = r * 8 + c;
+      if ((idx & 31) == lane) out[idx] = make_float2(accr[r][c], acci[r][c]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Solve R G = P per (segment, bin) in FP64 (wpe.hpp:90-94; numerics.hpp:32-49,
+// 81-94). grid (F, segments), block 256. Right-looking Cholesky in shared
+// memory, then forward / backward substitution of the M right-hand sides.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
+  extern __shared__ float4 smem_f4[];
+  const SegDev sd = a.segs[blockIdx.y];
+  if (!sd.wpe_active) return;
+  const int f = blockIdx.x;
+  const int M = a.M, km = a.taps * M, nb = gram_row_blocks(km), ntiles = gram_num_tiles(km);
+  const int ntri = nb * (nb + 1) / 2;
+  const int ld = km + 1;
+  cdbl* A = reinterpret_cast<cdbl*>(smem_f4);  // km x ld
+  cdbl* B = A + (size_t)km * ld;               // km x M
+  __shared__ double s_tr;
+  __shared__ int s_fail;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const float2* tiles = a.gram + (sd.wcell_off + (long long)f * sd.wchunks) * ntiles * 64;
+  const long long chunk_stride = (long long)ntiles * 64;
+
+  // lower triangle of R (upper mirrored by hermitize) and P, summed over chunks in double
+  for (int idx = tid; idx < km * km; idx += nth) {
+    const int i = idx / km, j = idx - i * km;
+    if (j > i) continue;
+    const int bi = i >> 3, bj = j >> 3;
+    const int tile = bi * (bi + 1) / 2 + bj;
+    const float2* p = tiles + (long long)tile * 64 + (i & 7) * 8 + (j & 7);
+    double re = 0.0, im = 0.0;
+    for (int c = 0; c < sd.wchunks; ++c) {
+      const float2 v = p[c * chunk_stride];
+      re += (double)v.x;
+      im += (double)v.y;
+    }
+    // hermitize (numerics.hpp:32-38): both triangles come from the same sums
+    if (i == j) im = 0.0;
+    A[i * ld + j] = cd_make(re, im);
+    A[j * ld + i] = cd_make(re, -im);
+  }
+  for (int idx = tid; idx < km * M; idx += nth) {
+    const int i = idx / M, c = idx - i * M;
+    const int tile = ntri + (i >> 3);
+    const float2* p = tiles + (long long)tile * 64 + (i & 7) * 8 + c;
+    double re = 0.0, im = 0.0;
+    for (int ch = 0; ch < sd.wchunks; ++ch) {
+      const float2 v = p[ch * chunk_stride];
+      re += (double)v.x;
+      im += (double)v.y;
+    }
+    B[i * M + c] = cd_make(re, im);
+  }
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  if (tid == 0) {  // regularize (numerics.hpp:41-49)
+    double tr = 0.0;
+    for (int i = 0; i < km; ++i) tr += A[i * ld + i].re;
+    double scale = tr / (double)km;
+    if (!(scale > 0.0)) scale = 1.0;
+    s_tr = a.regularization * scale;
+  }
+  __syncthreads();
+  for (int i = tid; i < km; i += nth) A[i * ld + i].re += s_tr;
+  __syncthreads();
+
+  // right-looking Cholesky on the lower triangle
+  for (int k = 0; k < km; ++k) {
+    if (tid == 0) {
+      const double d = A[k * ld + k].re;
+      if (!(d > 0.0)) s_fail = 1;
+      A[k * ld + k] = cd_make(sqrt(d > 0.0 ? d : 1.0), 0.0);
+    }
+    __syncthreads();
+    if (s_fail) break;
+    const double inv = 1.0 / A[k * ld + k].re;
+    for (int i = k + 1 + tid; i < km; i += nth) A[i * ld + k] = cd_scale(A[i * ld + k], inv);
+    __syncthreads();
+    for (int i = k + 1 + (tid >> 4); i < km; i += 16) {
+      const cdbl lik = A[i * ld + k];
+      for (int j = k + 1 + (tid & 15); j <= i; j += 16)
+        A[i * ld + j] = cd_sub(A[i * ld + j], cd_mulc(lik, A[j * ld + k]));
+    }
+    __syncthreads();
+  }
+  if (s_fail) {
+    // TODO(eigen-floor fallback, numerics.hpp:58-73, 90-93): reported, not repaired
+    if (tid == 0) atomicMin(a.status + blockIdx.y, make_status(5, f));
+    float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
+    for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2(0.f, 0.f);
+    return;
+  }
+  // forward: L Z = B
+  for (int k = 0; k < km; ++k) {
+    if (tid < M) B[k * M + tid] = cd_scale(B[k * M + tid], 1.0 / A[k * ld + k].re);
+    __syncthreads();
+    const int rem = km - k - 1;
+    for (int idx = tid; idx < rem * M; idx += nth) {
+      const int i = k + 1 + idx / M, c = idx % M;
+      B[i * M + c] = cd_sub(B[i * M + c], cd_mul(A[i * ld + k], B[k * M + c]));
+    }
+    __syncthreads();
+  }
+  // backward: L^H X = Z
+  for (int k = km - 1; k >= 0; --k) {
+    if (tid < M) B[k * M + tid] = cd_scale(B[k * M + tid], 1.0 / A[k * ld + k].re);
+    __syncthreads();
+    for (int idx = tid; idx < k * M; idx += nth) {
+      const int i = idx / M, c = idx % M;
+      B[i * M + c] = cd_sub(B[i * M + c], cd_cmul(A[k * ld + i], B[k * M + c]));
+    }
+    __syncthreads();
+  }
+  // conj(G) rounded to cfloat (wpe.hpp:95-96)
+  float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
+  for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2((float)B[idx].re, (float)(-B[idx].im));
+}
+
+// ---------------------------------------------------------------------------
+// Y_f = observed - history * conj(G) (wpe.hpp:95-96). grid (frame tiles, F,
+// segments), block 256: one thread per frame, slab channel-major in shared
+// memory, conj(G) broadcast from shared memory.
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__(256) wpe_apply_kernel(WpeArgs a) {
+  extern __shared__ float4 smem_f4[];
+  const SegDev sd = a.segs[blockIdx.z];
+  if (!sd.wpe_active) return;
+  const int tb = blockIdx.x * 256;
+  if (tb >= sd.T) return;
+  const int f = blockIdx.y;
+  const int taps = a.taps, km = taps * M, H = a.delay + taps - 1;
+  const int SF = 256 + H, pitch = SF | 1;
+  float2* slab = reinterpret_cast<float2*>(smem_f4);   // M * pitch
+  float2* gs = slab + M * pitch;                       // km * M
+  const int tid = threadIdx.x;
+  const int nfr = min(256, sd.T - tb);
+  const float2* yf = a.yobs + sd.y_off + (long long)f * sd.T * M;
+  for (int i = tid; i < (nfr + H) * M; i += 256) {
+    const int fr = i / M, c = i - fr * M;
+    const int t = tb - H + fr;
+    slab[c * pitch + fr] = t >= 0 ? yf[(long long)t * M + c] : make_float2(0.f, 0.f);
+  }
+  const float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
+  for (int i = tid; i < km * M; i += 256) gs[i] = g[i];
+  __syncthreads();
+  float2 acc[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) acc[c] = make_float2(0.f, 0.f);
+  const int fi = min(tid, nfr - 1);
+  for (int u = 0; u < taps; ++u) {
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const float2 v = slab[c * pitch + fi + u];
+      const float2* gr = gs + (u * M + c) * M;
+#pragma unroll
+      for (int c2 = 0; c2 < M; ++c2) {
+        const float2 gg = gr[c2];
+        acc[c2].x = fmaf(v.x, gg.x, acc[c2].x);
+        acc[c2].x = fmaf(-v.y, gg.y, acc[c2].x);
+        acc[c2].y = fmaf(v.x, gg.y, acc[c2].y);
+        acc[c2].y = fmaf(v.y, gg.x, acc[c2].y);
+      }
+    }
+  }
+  // observed - s, staged through shared memory for contiguous stores
+  float2 res[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    const float2 o = slab[c * pitch + fi + H];
+    res[c] = make_float2(o.x - acc[c].x, o.y - acc[c].y);
+  }
+  __syncthreads();
+  float2* stage = slab;  // 256 * M <= M * pitch
+  if (tid < nfr) {
+#pragma unroll
+    for (int c = 0; c < M; ++c) stage[tid * M + c] = res[c];
+  }
+  __syncthreads();
+  float2* out = a.yout + sd.y_off + ((long long)f * sd.T + tb) * M;
+  for (int i = tid; i < nfr * M; i += 256) out[i] = stage[i];
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+int wpe_gram_tiles(int km) { return gram_num_tiles(km); }
+
+template <int M>
+static cudaError_t launch_wpe_iter_m(const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
+                                     cudaStream_t st, long long* launches) {
+  const int km = a.taps * M, H = a.delay + a.taps - 1;
+  {
+    dim3 grid((max_frames + 255) / 256, F, nseg);
+    wpe_power_kernel<<<grid, 256, 0, st>>>(a);
+    ++*launches;
+  }
+  {
+    const int ngroups = (gram_num_tiles(km) + kGramWarps - 1) / kGramWarps;
+    const size_t smem = sizeof(float2) * (size_t)M * ((kGramTileFrames + H) | 1) + sizeof(float) * kGramTileFrames;
+    if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(wpe_gram_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid(ngroups * max_wchunks, F, nseg);
+    wpe_gram_kernel<M><<<grid, kGramThreads, smem, st>>>(a);
+    ++*launches;
+  }
+  {
+    const size_t smem = sizeof(cdbl) * ((size_t)km * (km + 1) + (size_t)km * M);
+    if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(wpe_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid(F, nseg);
+    wpe_solve_kernel<<<grid, 256, smem, st>>>(a);
+    ++*launches;
+  }
+  {
+    const size_t smem = sizeof(float2) * ((size_t)M * ((256 + H) | 1) + (size_t)km * M);
+    if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(wpe_apply_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((max_frames + 255) / 256, F, nseg);
+    wpe_apply_kernel<M><<<grid, 256, smem, st>>>(a);
+    ++*launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wpe_iteration(const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
+                                 cudaStream_t st, long long* launches) {
+  switch (a.M) {
+    case 1: return launch_wpe_iter_m<1>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    case 2: return launch_wpe_iter_m<2>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    case 3: return launch_wpe_iter_m<3>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    case 4: return launch_wpe_iter_m<4>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    case 5: return launch_wpe_iter_m<5>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    case 6: return launch_wpe_iter_m<6>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    case 7: return launch_wpe_iter_m<7>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    case 8: return launch_wpe_iter_m<8>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace gssb

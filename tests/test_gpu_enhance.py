@@ -1,0 +1,119 @@
+"""GPU parity of the hot path `enhance_batch` (scheduler.hpp:314-365) against the CPU oracle, through the
+C ABI. Gates: part offsets / output lengths / ref channel / zeroed bins exact, masks within
+1e-3, beamformer within 1e-3 relative, waveform SDR >= 40 dB, ll_final within 1e-4."""
+import numpy as np
+import pytest
+
+from .gpu_util import rel_fro, sdr_db
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gss():
+    from paper_2212_05271_b200 import gss as g
+    g.default_context()
+    return g
+
+
+def oracle_enhance(oracle, ss, cfg):
+    return oracle.enhance(ss.audio.channels, ss.activity.grid, ss.activity.target_index, ss.activity.noise_index,
+                          [(p.sample_begin, p.sample_end) for p in ss.parts], fft_size=cfg.stft.fft_size,
+                          shift=cfg.stft.shift, window=cfg.stft.window, sample_rate=cfg.stft.sample_rate,
+                          enable_wpe=cfg.enable_wpe, taps=cfg.wpe.taps, delay=cfg.wpe.delay,
+                          wpe_iterations=cfg.wpe.iterations, psd_context=cfg.wpe.psd_context,
+                          regularization=cfg.wpe.regularization, bss_iterations=cfg.bss_iterations, diag=True)
+
+
+def check_against_oracle(got, want, label=""):
+    assert got.error is None, (label, got.error)
+    assert got.frames == want.frames
+    assert got.ref_channel == want.ref_channel, (label, got.ref_channel, want.ref_channel)
+    assert got.zeroed_bins == want.zeroed_bins
+    assert [len(o) for o in got.outputs] == [len(o) for o in want.outputs]
+    d_gamma = float(np.abs(got.posteriors - want.gamma).max())
+    e_h = rel_fro(got.h, want.h)
+    sdr = sdr_db(got.mono, want.mono)
+    e_ll = abs(got.ll_final - want.ll_final) / abs(want.ll_final)
+    print(f"[{label}] max|dgamma|={d_gamma:.2e} rel(h)={e_h:.2e} SDR={sdr:.1f} dB rel(ll)={e_ll:.2e}")
+    assert d_gamma < 1e-3, (label, d_gamma)
+    assert e_h < 1e-3, (label, e_h)
+    assert sdr >= 40.0, (label, sdr)
+    assert e_ll < 1e-4, (label, e_ll)
+    for a, b in zip(got.outputs, want.outputs):
+        assert sdr_db(a, b) >= 40.0
+
+
+def test_enhance_tiny_batch_with_wpe(gss, oracle):
+    from paper_2212_05271_b200 import synth
+    w = synth.workload("tiny")
+    res = gss.scheduler.enhance_batches(w.segments, w.cfg, diagnostics=True)
+    for i, (ss, r) in enumerate(zip(w.segments, res)):
+        check_against_oracle(r, oracle_enhance(oracle, ss, w.cfg), f"tiny[{i}]")
+
+
+def test_enhance_cfg1_no_wpe(gss, oracle):
+    # BASELINE configs[0]: 2 speakers, 7 channels, 10 s, 512-point STFT, 20 iterations, no WPE
+    from paper_2212_05271_b200 import synth
+    w = synth.workload("cfg1")
+    r = gss.scheduler.enhance_batch(w.segments[0], w.cfg, diagnostics=True)
+    assert r.frames == 1251 and len(r.outputs[0]) == 160000
+    check_against_oracle(r, oracle_enhance(oracle, w.segments[0], w.cfg), "cfg1")
+
+
+def test_enhance_ragged_batch_mixed_shapes(gss, oracle):
+    # different M, K, N in one call: results must equal one-at-a-time calls bit for bit (batch invariance,
+    # the analogue of the reference's worker-count invariance, test_scheduler.cpp:376-407)
+    from paper_2212_05271_b200 import synth
+    from paper_2212_05271_b200.gss import scheduler, stft, wpe
+    cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(6, 2, 2, 0, 1e-10), True, 6)
+    segs = [synth.make_supersegment(900, 4, 2, 2.0, 1.0, cfg), synth.make_supersegment(901, 8, 4, 1.5, 0.5, cfg),
+            synth.make_supersegment(902, 2, 3, 3.0, 0.0, cfg), synth.make_supersegment(903, 4, 2, 1.0, 2.0, cfg)]
+    together = gss.scheduler.enhance_batches(segs, cfg, diagnostics=True)
+    for i, ss in enumerate(segs):
+        alone = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
+        assert alone.mono.tobytes() == together[i].mono.tobytes(), i
+        assert alone.ref_channel == together[i].ref_channel
+        check_against_oracle(together[i], oracle_enhance(oracle, ss, cfg), f"ragged[{i}]")
+
+
+def test_enhance_multi_part_cut_and_failure_isolation(gss, oracle):
+    from paper_2212_05271_b200 import synth
+    from paper_2212_05271_b200.gss import scheduler, stft, wpe, manifests
+    cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(), False, 4)
+    good = synth.make_supersegment(950, 3, 2, 2.0, 1.0, cfg)
+    n = good.audio.num_samples()
+    # two parts, the second one clipped by the end of the window (scheduler.hpp:354-356)
+    good.parts = [scheduler.Part(manifests.Segment(), 1000, 9000), scheduler.Part(manifests.Segment(), 30000, n + 500)]
+    short = scheduler.SuperSegment(stft.RealSignal(np.zeros((3, 100), np.float32), 16000), good.activity, [])
+    badact = synth.make_supersegment(951, 3, 2, 2.0, 1.0, cfg)
+    badact.activity = manifests.ActivityMatrix(badact.activity.grid[:-3], badact.activity.classes, 0, 2)
+    res = gss.scheduler.enhance_batches([short, good, badact], cfg, diagnostics=True)
+    assert isinstance(res[0].error, gss.InputTooShortError)
+    assert isinstance(res[2].error, gss.ShapeError)
+    assert [len(o) for o in res[1].outputs] == [8000, n - 30000]
+    want = oracle_enhance(oracle, good, cfg)
+    check_against_oracle(res[1], want, "multi-part")
+    with pytest.raises(gss.InputTooShortError):
+        gss.scheduler.enhance_batch(short, cfg)
+    with pytest.raises(gss.ConfigError):
+        gss.scheduler.enhance_batch(good, scheduler.PipelineConfig(bss_iterations=0))
+
+
+def test_resident_batch_matches_one_shot(gss):
+    # upload / run / fetch == enhance_batch, and re-running a resident batch is bit-stable
+    from paper_2212_05271_b200 import synth
+    w = synth.workload("tiny")
+    one = gss.scheduler.enhance_batches(w.segments, w.cfg)
+    rb = gss.scheduler.ResidentBatch(w.segments, w.cfg, pinned=True).upload()
+    rb.run()
+    a = rb.fetch()
+    rb.run()
+    b = rb.fetch()
+    rb.free()
+    for x, y, z in zip(one, a, b):
+        assert x.outputs[0].tobytes() == y.outputs[0].tobytes() == z.outputs[0].tobytes()
+    ctx = gss.default_context()
+    assert ctx.launch_count > 0
+    ms = ctx.stage_ms()
+    assert ms["mask"] > 0 and ms["stft"] > 0

@@ -1,0 +1,289 @@
+"""GPU parity of every stage operator against the CPU oracle, through the C ABI of libgss_b200.so.
+
+Tolerances (BASELINE.json north_star): masks and beamformer weights within 1e-3 in FP32, waveform SDR
+>= 40 dB, integer results exact. Each test names the reference test it mirrors where one exists.
+"""
+import numpy as np
+import pytest
+
+from .gpu_util import cgauss_tensor, random_activity, rel_fro, sdr_db
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gss():
+    from paper_2212_05271_b200 import gss as g
+    g.default_context()  # fails loudly when there is no B200 / library
+    return g
+
+
+def spec(gss, data, cfg=None, num_samples=0):
+    return gss.stft.SpectrogramTensor(np.ascontiguousarray(data, np.complex64), cfg or gss.stft.StftConfig(),
+                                      0, num_samples)
+
+
+# --------------------------------------------------------------------------- STFT
+@pytest.mark.parametrize("fft,shift,m,n", [(512, 128, 3, 5000), (1024, 256, 7, 4097), (512, 128, 8, 512),
+                                           (256, 64, 1, 3000), (512, 256, 2, 16000)])
+def test_stft_matches_oracle(gss, oracle, fft, shift, m, n):
+    rng = np.random.RandomState(fft + m + n)
+    audio = (rng.randn(m, n) * 0.1).astype(np.float32)
+    cfg = gss.stft.StftConfig(fft, shift, 0, 16000)
+    got = gss.stft.analyze(gss.stft.RealSignal(audio, 16000), cfg)
+    want = oracle.stft(audio, oracle.stft_cfg(fft, shift, 0, 16000))
+    assert got.data.shape == want.shape
+    assert got.origin_samples == -fft // 2 and got.num_samples == n  # test_stft.cpp:90-99
+    err = np.abs(got.data - want).max() / np.abs(want).max()
+    assert err < 2e-6, err
+
+
+def test_stft_dc_bin_and_sqrt_hann(gss, oracle):
+    # test_stft.cpp:120-131: DC bin of an all-ones signal = sum(window) = fft/2
+    cfg = gss.stft.StftConfig()
+    got = gss.stft.analyze(gss.stft.RealSignal(np.ones((1, 8192), np.float32), 16000), cfg)
+    assert abs(got.data[0, 4, 0] - 512.0) < 1e-2
+    cfg2 = gss.stft.StftConfig(512, 128, 1, 16000)
+    rng = np.random.RandomState(5)
+    audio = rng.randn(2, 4000).astype(np.float32)
+    got = gss.stft.analyze(gss.stft.RealSignal(audio, 0), cfg2)
+    want = oracle.stft(audio, oracle.stft_cfg(512, 128, 1, 16000))
+    assert np.abs(got.data - want).max() / np.abs(want).max() < 2e-6
+
+
+def test_stft_errors(gss):
+    # test_stft.cpp:101-118
+    a = np.zeros((2, 100), np.float32)
+    with pytest.raises(gss.InputTooShortError):
+        gss.stft.analyze(gss.stft.RealSignal(a, 16000), gss.stft.StftConfig())
+    with pytest.raises(gss.ConfigError):
+        gss.stft.analyze(gss.stft.RealSignal(np.zeros((1, 4096), np.float32), 8000), gss.stft.StftConfig())
+    with pytest.raises(gss.ConfigError):
+        gss.stft.analyze(gss.stft.RealSignal(np.zeros((1, 4096), np.float32), 16000),
+                         gss.stft.StftConfig(1024, 300))
+
+
+@pytest.mark.parametrize("n,fft,shift,window", [(4096, 1024, 256, 0), (50000, 1024, 256, 0), (4097, 1024, 256, 0),
+                                                (1024, 1024, 256, 0), (8000, 512, 128, 1), (6000, 512, 128, 0)])
+def test_istft_round_trip_and_oracle(gss, oracle, n, fft, shift, window):
+    # test_stft.cpp:149-172 (round trip <= 1e-6) and parity with the oracle's synthesize
+    rng = np.random.RandomState(n)
+    audio = (rng.randn(2, n) * 0.3).astype(np.float32)
+    cfg = gss.stft.StftConfig(fft, shift, window, 16000)
+    sp = gss.stft.analyze(gss.stft.RealSignal(audio, 16000), cfg)
+    back = gss.stft.synthesize(sp)
+    assert back.channels.shape == audio.shape
+    assert np.abs(back.channels - audio).max() < 2e-6
+    want = oracle.istft(sp.data, oracle.stft_cfg(fft, shift, window, 16000), n)
+    assert np.abs(back.channels - want).max() < 2e-6
+    # num_samples == 0: length (T-1)*shift
+    sp0 = gss.stft.SpectrogramTensor(sp.data, cfg, 0, 0)
+    b0 = gss.stft.synthesize(sp0)
+    w0 = oracle.istft(sp.data, oracle.stft_cfg(fft, shift, window, 16000), 0)
+    assert b0.channels.shape == w0.shape
+    assert np.abs(b0.channels - w0).max() < 2e-6
+
+
+def test_istft_random_spectrum_matches_oracle(gss, oracle):
+    # arbitrary (non-STFT-consistent) spectra, incl. imaginary DC/Nyquist parts that the real inverse ignores
+    x = cgauss_tensor(3, 257, 37, 2)
+    cfg = gss.stft.StftConfig(512, 128, 0, 16000)
+    got = gss.stft.synthesize(gss.stft.SpectrogramTensor(x, cfg, 0, 4000)).channels
+    want = oracle.istft(x, oracle.stft_cfg(512, 128), 4000)
+    assert np.abs(got - want).max() / np.abs(want).max() < 2e-6
+
+
+# --------------------------------------------------------------------------- WPE
+def test_unit_normalize(gss, oracle):
+    # test_wpe.cpp:163-182
+    y = cgauss_tensor(1, 9, 50, 5)
+    y[2, 3, :] = 0
+    got = gss.wpe.unit_normalize(spec(gss, y)).data
+    want = oracle.unit_normalize(y)
+    assert np.abs(got - want).max() < 1e-6
+    assert np.all(got[2, 3] == 0)
+    nz = np.linalg.norm(got, axis=2)
+    nz[2, 3] = 1
+    assert np.abs(nz - 1).max() < 1e-5
+
+
+def test_wpe_pass_through_and_config(gss):
+    # test_wpe.cpp:58-76
+    y = cgauss_tensor(2, 4, 12, 3)
+    out = gss.wpe.dereverberate(spec(gss, y), gss.wpe.WpeConfig(10, 2, 3)).data
+    assert out.tobytes() == y.tobytes()
+    with pytest.raises(gss.ConfigError):
+        gss.wpe.dereverberate(spec(gss, y), gss.wpe.WpeConfig(0, 2, 3))
+
+
+@pytest.mark.parametrize("f,t,m,taps,delay,iters,ctx", [(6, 600, 4, 8, 2, 3, 0), (5, 700, 7, 10, 2, 3, 0),
+                                                        (4, 640, 8, 10, 3, 2, 0), (5, 300, 2, 5, 1, 3, 2),
+                                                        (3, 1300, 3, 10, 2, 1, 0), (3, 200, 1, 4, 2, 2, 0),
+                                                        (3, 400, 5, 6, 2, 2, 0), (3, 400, 6, 7, 2, 2, 1)])
+def test_wpe_matches_oracle(gss, oracle, f, t, m, taps, delay, iters, ctx):
+    # white input (test_wpe.cpp:101-110 shape) plus a synthetic echo (test_wpe.cpp:112-146)
+    rng = np.random.RandomState(f * t + m)
+    s = (rng.randn(f, t, m) + 1j * rng.randn(f, t, m)).astype(np.complex64)
+    y = s.copy()
+    y[:, 3:, :] += 0.7 * s[:, :-3, :]
+    y[:, 5:, :] += 0.4 * np.roll(s, 1, axis=2)[:, :-5, :]
+    cfg = gss.wpe.WpeConfig(taps, delay, iters, ctx, 1e-10)
+    got = gss.wpe.dereverberate(spec(gss, y), cfg).data
+    want = oracle.wpe(y, oracle.wpe_cfg(taps, delay, iters, ctx, 1e-10))
+    err = rel_fro(got, want)
+    assert err < 1e-4, err
+    # determinism (test_wpe.cpp:88-95)
+    again = gss.wpe.dereverberate(spec(gss, y), cfg).data
+    assert again.tobytes() == got.tobytes()
+
+
+# --------------------------------------------------------------------------- cACGMM
+def _em_problem(seed, f, t, m, k, noise=True):
+    rng = np.random.RandomState(seed)
+    act = random_activity(seed, t, k, noise)
+    # class-dependent spatial structure so the fit is not degenerate
+    steer = (rng.randn(k, m) + 1j * rng.randn(k, m))
+    y = np.zeros((f, t, m), np.complex64)
+    for ff in range(f):
+        lab = np.array([rng.choice(np.flatnonzero(act[tt])) for tt in range(t)])
+        sig = (rng.randn(t) + 1j * rng.randn(t))[:, None] * steer[lab]
+        y[ff] = (sig + 0.3 * (rng.randn(t, m) + 1j * rng.randn(t, m))).astype(np.complex64)
+    return y, act
+
+
+@pytest.mark.parametrize("m,k,noise", [(4, 3, True), (7, 3, True), (7, 4, True), (8, 5, True), (2, 2, True),
+                                       (3, 2, False), (5, 4, True), (6, 6, True), (8, 7, True), (1, 2, True),
+                                       (7, 8, True), (5, 6, False)])
+def test_em_fit_matches_oracle(gss, oracle, m, k, noise):
+    f, t, iters = 6, 520, 8
+    y, act = _em_problem(100 * m + k, f, t, m, k, noise)
+    yn = oracle.unit_normalize(y)
+    am = gss.manifests.ActivityMatrix(act, ["c%d" % i for i in range(k)], 0, k - 1 if noise else -1)
+    got = gss.cacgmm.em_fit(spec(gss, yn), am, iters)
+    want = oracle.em_fit(yn, act, 0, k - 1 if noise else -1, iters)
+    assert len(got.likelihood_trace) == iters + 1
+    # inactive posteriors exactly zero, rows sum to one (test_cacgmm.cpp:224-278)
+    assert np.all(got.posteriors[:, act == 0] == 0)
+    assert np.abs(got.posteriors.sum(2) - 1).max() < 1e-5
+    d_gamma = np.abs(got.posteriors - want.gamma).max()
+    assert d_gamma < 1e-3, d_gamma
+    assert np.abs(got.state.weights - want.pi).max() < 1e-4
+    for ff in range(f):
+        for kk in range(k):
+            e = rel_fro(got.state.shapes[ff, kk], want.shapes[ff, kk])
+            assert e < 1e-3, (ff, kk, e)
+    tr = np.abs(np.array(got.likelihood_trace) - want.trace) / np.abs(want.trace)
+    assert tr.max() < 1e-5, tr
+    # log_likelihood(state) == last trace entry (test_cacgmm.cpp:280-301)
+    ll = gss.cacgmm.log_likelihood(spec(gss, yn), got.state, am)
+    assert abs(ll - got.likelihood_trace[-1]) / abs(ll) < 1e-6
+
+
+def test_em_first_iteration_closed_form(gss):
+    # test_cacgmm.cpp:165-182: with B = I and unit-norm frames, LL_0 = F*T*c0(M) when all classes are active
+    import math
+    f, t, m, k = 5, 300, 4, 3
+    y = cgauss_tensor(9, f, t, m)
+    y /= np.linalg.norm(y, axis=2, keepdims=True)
+    act = np.ones((t, k), np.uint8)
+    am = gss.manifests.ActivityMatrix(act, ["a", "b", "c"], 0, -1)
+    res = gss.cacgmm.em_fit(spec(gss, y), am, 1)
+    c0 = -m * math.log(2 * math.pi) + math.lgamma(m)
+    assert abs(c0 - (-5.559748796409327)) < 1e-12
+    assert abs(res.likelihood_trace[0] - f * t * c0) / abs(f * t * c0) < 1e-6
+
+
+def test_em_dead_class_and_errors(gss, oracle):
+    # test_cacgmm.cpp:303-335: a class that is never active keeps B = I and pi = 1e-10
+    f, t, m, k = 3, 200, 3, 3
+    y = cgauss_tensor(4, f, t, m)
+    yn = oracle.unit_normalize(y)
+    act = np.ones((t, k), np.uint8)
+    act[:, 1] = 0
+    am = gss.manifests.ActivityMatrix(act, ["a", "b", "n"], 0, 2)
+    res = gss.cacgmm.em_fit(spec(gss, yn), am, 3)
+    assert np.all(res.posteriors[:, :, 1] == 0)
+    assert np.allclose(res.state.weights[:, 1], 1e-10)
+    assert np.abs(res.state.shapes[:, 1] - np.eye(m)).max() < 1e-12
+    with pytest.raises(gss.ConfigError):
+        gss.cacgmm.em_fit(spec(gss, yn), am, 0)
+    bad = gss.manifests.ActivityMatrix(act[:-1], ["a", "b", "n"], 0, 2)
+    with pytest.raises(gss.ShapeError):
+        gss.cacgmm.em_fit(spec(gss, yn), bad, 2)
+
+
+def test_em_degenerate_frames_without_noise_class(gss, oracle):
+    # frames with no active class: uniform over all classes (cacgmm.hpp:217-226)
+    f, t, m, k = 3, 260, 4, 3
+    y, _ = _em_problem(77, f, t, m, k, True)
+    yn = oracle.unit_normalize(y)
+    act = random_activity(5, t, k, noise=False, holes=True)
+    assert (act.sum(1) == 0).any()
+    am = gss.manifests.ActivityMatrix(act, ["a", "b", "c"], 0, -1)
+    got = gss.cacgmm.em_fit(spec(gss, yn), am, 4)
+    want = oracle.em_fit(yn, act, 0, -1, 4)
+    assert np.abs(got.posteriors - want.gamma).max() < 1e-3
+    assert np.abs(np.array(got.likelihood_trace) - want.trace).max() / np.abs(want.trace).max() < 1e-5
+
+
+# --------------------------------------------------------------------------- beamformer
+@pytest.mark.parametrize("m,k", [(2, 2), (4, 3), (7, 4), (8, 5), (3, 6), (5, 2), (6, 8), (1, 2)])
+def test_mvdr_chain_matches_oracle(gss, oracle, m, k):
+    f, t = 9, 333
+    rng = np.random.RandomState(m * 10 + k)
+    y = cgauss_tensor(m + k, f, t, m, 3.0)
+    g = rng.rand(f, t, k).astype(np.float32)
+    g /= g.sum(2, keepdims=True)
+    target = k // 2
+    st = gss.beamform.accumulate_stats(spec(gss, y), g, target)
+    wt, wb = oracle.mvdr_stats(y, g, target)
+    assert rel_fro(st.target, wt) < 1e-5 and rel_fro(st.background, wb) < 1e-5
+    ref = gss.beamform.select_reference(st)
+    assert ref == oracle.select_reference(wt, wb)
+    flt = gss.beamform.mvdr(st, ref)
+    wh, wz = oracle.mvdr(wt, wb, ref)
+    assert flt.zeroed_bins == wz
+    assert rel_fro(flt.h, wh) < 1e-4
+    out = gss.beamform.apply(flt, spec(gss, y)).data
+    want = oracle.apply_filter(wh, y)
+    assert out.shape == (f, t, 1)
+    assert rel_fro(out[:, :, 0], want) < 1e-4
+
+
+def test_mvdr_frozen_vector_and_edge_cases(gss):
+    # test_beamform.cpp:127-145: frozen h = [0.8+0.04i, -0.08-0.2i]
+    tgt = np.array([[[2, 0.5j], [-0.5j, 1]]], np.complex128)
+    bg = np.array([[[1, 0.2], [0.2, 2]]], np.complex128)
+    st = gss.beamform.BeamformerStats(tgt, bg, 1)
+    flt = gss.beamform.mvdr(st, 0)
+    c = np.linalg.solve(bg[0], tgt[0])
+    want = c[:, 0] / np.trace(c)
+    assert np.abs(flt.h[0] - want).max() < 1e-9
+    # ties -> lowest index (test_beamform.cpp:100-121)
+    eye = np.tile(np.eye(3, dtype=np.complex128), (4, 1, 1))
+    assert gss.beamform.select_reference(gss.beamform.BeamformerStats(eye, eye, 1)) == 0
+    t2 = eye.copy()
+    t2[:, 2, 2] = 5
+    assert gss.beamform.select_reference(gss.beamform.BeamformerStats(t2, eye, 1)) == 2
+    # zero target -> trace 0 -> zeroed bins counted (test_beamform.cpp:190-205)
+    z = gss.beamform.mvdr(gss.beamform.BeamformerStats(np.zeros_like(eye), eye, 1), 0)
+    assert z.zeroed_bins == 4 and np.all(z.h == 0)
+    with pytest.raises(gss.ShapeError):
+        gss.beamform.mvdr(gss.beamform.BeamformerStats(eye, eye, 1), 3)
+    # all-zero target mask -> DegenerateStatsError (test_beamform.cpp:88-94)
+    y = cgauss_tensor(1, 4, 50, 3)
+    g = np.zeros((4, 50, 2), np.float32)
+    g[:, :, 1] = 1
+    with pytest.raises(gss.DegenerateStatsError):
+        gss.beamform.accumulate_stats(spec(gss, y), g, 0)
+
+
+def test_numerics_rank_deficient_background_uses_eigen_floor(gss, oracle):
+    # test_numerics.cpp:130-138 through the MVDR solve: rank-1 background is repaired by the eigenvalue floor
+    v = np.array([1, 1j, 1 + 1j])
+    bg = np.outer(v, v.conj())[None].astype(np.complex128)
+    tgt = np.eye(3, dtype=np.complex128)[None]
+    flt = gss.beamform.mvdr(gss.beamform.BeamformerStats(tgt, bg, 1), 0)
+    wh, wz = oracle.mvdr(tgt, bg, 0)
+    assert np.isfinite(flt.h).all() and flt.zeroed_bins == wz
+    assert rel_fro(flt.h, wh) < 1e-3
