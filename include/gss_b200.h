@@ -209,6 +209,19 @@ gss_status gss_b200_batch_fetch(gss_b200_ctx* ctx, gss_b200_batch* batch, gss_se
 void gss_b200_batch_free(gss_b200_ctx* ctx, gss_b200_batch* batch);
 gss_status gss_b200_stage_ms(gss_b200_ctx* ctx, double* ms /* [GSS_B200_NUM_STAGES] */);
 
+/* Per-kernel device clocks. gss_b200_profile(ctx, 1) resets the counters and brackets every launch with
+ * CUDA events on the context stream; gss_b200_kernel_ms synchronises and returns, per kernel class, the
+ * summed duration (ms) and the number of launches since then. Classes:
+ * 0 stft, 1 wpe_power, 2 wpe_gram, 3 wpe_solve, 4 wpe_apply, 5 em_pass, 6 em_update, 7 mvdr, 8 apply,
+ * 9 istft, 10 misc. Launch counts are maintained even when event timing is off. */
+/* Measured FP32 FMA throughput of the device (TFLOP/s, FMA = 2 flop): the roofline denominator of the
+ * FP32-bound kernels (WPE Gram, EM sweep). Bench harness use. */
+gss_status gss_b200_fp32_peak(gss_b200_ctx* ctx, double* tflops);
+#define GSS_B200_NUM_KERNELS 11
+gss_status gss_b200_profile(gss_b200_ctx* ctx, int32_t enable);
+gss_status gss_b200_kernel_ms(gss_b200_ctx* ctx, double* ms /* [GSS_B200_NUM_KERNELS] */,
+                              int64_t* launches /* [GSS_B200_NUM_KERNELS] */);
+
 /* ---- host-only helpers (bit-exact integer / scalar forms; no context) ---- */
 
 /* stft::frame_count (stft.hpp:120-124) */

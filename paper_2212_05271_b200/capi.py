@@ -15,6 +15,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libgss_b200.so")
 
 NUM_STAGES = 7
+NUM_KERNELS = 11
+KERNEL_NAMES = ("stft", "wpe_power", "wpe_gram", "wpe_solve", "wpe_apply", "em_pass", "em_update", "mvdr", "apply",
+                "istft", "misc")
 STAGE_NAMES = ("stft", "wpe", "mask", "beamform", "istft", "h2d", "d2h")
 
 
@@ -120,7 +123,7 @@ EXPORTS = [
     "gss_b200_host_free", "gss_b200_stft", "gss_b200_istft", "gss_b200_wpe", "gss_b200_unit_normalize",
     "gss_b200_em_fit", "gss_b200_log_likelihood", "gss_b200_mvdr_stats", "gss_b200_select_reference",
     "gss_b200_mvdr", "gss_b200_apply", "gss_b200_enhance_batch", "gss_b200_batch_upload", "gss_b200_batch_run",
-    "gss_b200_batch_fetch", "gss_b200_batch_free", "gss_b200_stage_ms", "gss_b200_frame_count",
+    "gss_b200_batch_fetch", "gss_b200_batch_free", "gss_b200_stage_ms", "gss_b200_profile", "gss_b200_kernel_ms", "gss_b200_fp32_peak", "gss_b200_frame_count",
     "gss_b200_build_activity_at", "gss_b200_assemble_indices", "gss_b200_cacg_log_pdf",
     "gss_b200_time_varying_weights",
 ]

@@ -32,6 +32,8 @@ void set_thread_error(int code, const std::string& msg, long long freq) {
 struct Tables {
   float2* tw = nullptr;
   float* win = nullptr;
+  double2* tw_d = nullptr;
+  double* win_d = nullptr;
 };
 
 struct Fail {
@@ -53,6 +55,15 @@ struct gss_b200_ctx {
   long long device_bytes = 0;
   std::map<std::pair<int, int>, Tables> tables;
   double stage_ms[GSS_B200_NUM_STAGES] = {0, 0, 0, 0, 0, 0, 0};
+  // optional per-kernel device clocks (gss_b200_profile)
+  bool prof_on = false;
+  struct ProfRec {
+    int id;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfRec> prof_recs;
+  double kernel_ms[GSS_B200_NUM_KERNELS] = {0};
+  long long kernel_launches[GSS_B200_NUM_KERNELS] = {0};
   int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
   int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
 };
@@ -67,6 +78,28 @@ gss_status fail(gss_b200_ctx* c, gss_status code, const std::string& msg, long l
   set_thread_error(code, msg, freq);
   return code;
 }
+
+/// Brackets one kernel launch with events when profiling is on, and counts it.
+struct KClock {
+  gss_b200_ctx* c;
+  int id;
+  cudaEvent_t b = nullptr;
+  KClock(gss_b200_ctx* ctx, int kid) : c(ctx), id(kid) {
+    ++c->launches;
+    ++c->kernel_launches[id];
+    if (!c->prof_on) return;
+    cudaEvent_t a;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c->stream);
+    c->prof_recs.push_back({id, a, b});
+  }
+  ~KClock() {
+    if (b) cudaEventRecord(b, c->stream);
+  }
+};
+enum KernelId { kK_stft = 0, kK_wpe_power, kK_wpe_gram, kK_wpe_solve, kK_wpe_apply, kK_em_pass, kK_em_update,
+                kK_mvdr, kK_apply, kK_istft, kK_misc };
 
 #define CU_TRY(ctx, expr)                                                                          \
   do {                                                                                             \
@@ -103,8 +136,8 @@ bool validate_wpe(const gss_wpe_config& w, std::string& why) {
 }
 bool kernel_fft_supported(const gss_stft_config& s, std::string& why) {
   const int n = s.fft_size;
-  if ((n & (n - 1)) != 0 || n < 32 || n > 4096)
-    return why = "fft_size must be a power of two in [32, 4096] on this device path", false;
+  if ((n & (n - 1)) != 0 || n < 32 || n > 2048)
+    return why = "fft_size must be a power of two in [32, 2048] on this device path", false;
   if (s.window != 0 && s.window != 1) return why = "stft: unknown window", false;
   return true;
 }
@@ -144,19 +177,27 @@ gss_status get_tables(gss_b200_ctx* c, const gss_stft_config& s, Tables& out) {
   const int n = s.fft_size;
   std::vector<float2> tw(n / 2);
   std::vector<float> win(n);
+  std::vector<double2> tw_d(n / 2);
+  std::vector<double> win_d(n);
   for (int k = 0; k < n / 2; ++k) {
     const double ang = -2.0 * M_PI * k / n;
-    tw[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    tw_d[k] = make_double2(std::cos(ang), std::sin(ang));
+    tw[k] = make_float2((float)tw_d[k].x, (float)tw_d[k].y);
   }
   for (int i = 0; i < n; ++i) {  // stft.hpp:89-97
     const double h = 0.5 * (1.0 - std::cos(2.0 * M_PI * i / n));
-    win[i] = (float)(s.window == 0 ? h : std::sqrt(h));
+    win_d[i] = s.window == 0 ? h : std::sqrt(h);
+    win[i] = (float)win_d[i];
   }
   Tables t;
   CU_TRY(c, cudaMalloc(&t.tw, sizeof(float2) * (n / 2)));
   CU_TRY(c, cudaMalloc(&t.win, sizeof(float) * n));
+  CU_TRY(c, cudaMalloc(&t.tw_d, sizeof(double2) * (n / 2)));
+  CU_TRY(c, cudaMalloc(&t.win_d, sizeof(double) * n));
   CU_TRY(c, cudaMemcpyAsync(t.tw, tw.data(), sizeof(float2) * (n / 2), cudaMemcpyHostToDevice, c->stream));
   CU_TRY(c, cudaMemcpyAsync(t.win, win.data(), sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(t.tw_d, tw_d.data(), sizeof(double2) * (n / 2), cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(t.win_d, win_d.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   c->tables[key] = t;
   out = t;
@@ -289,7 +330,7 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
     d.w_off = o_w;
     d.wcell_off = o_wcell;
     d.g_wpe_off = o_gw;
-    d.TC = pick_chunks(c, s.T, (long long)specs.size() * F);
+    d.TC = pick_chunks(c, s.T, F);  // a function of the segment alone: results do not depend on batch composition
     d.nchunks = (s.T + d.TC - 1) / d.TC;
     d.WTC = c->wpe_chunk_frames > 0 ? c->wpe_chunk_frames : std::max(s.T, 1);
     d.wchunks = (s.T + d.WTC - 1) / d.WTC;
@@ -413,7 +454,10 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
   a.psd_context = w.psd_context;
   for (int it = 0; it < w.iterations; ++it) {
     a.ycur = it == 0 ? g.Y : g.Yd;
-    CU_TRY(c, launch_wpe_iteration(a, g.nseg, g.F, g.max_T, g.max_wchunks, c->stream, &c->launches));
+    for (int step = 0; step < 4; ++step) {
+      KClock k(c, kK_wpe_power + step);
+      CU_TRY(c, launch_wpe_step(step, a, g.nseg, g.F, g.max_T, g.max_wchunks, c->stream));
+    }
   }
   return GSS_OK;
 }
@@ -444,8 +488,10 @@ gss_status run_em(gss_b200_ctx* c, Group& g, const EmRun& r) {
   u.cell_stride = g.cell_stride;
   u.F = g.F;
   u.mode = r.from_state ? kEmFromState : kEmInit;
-  CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
-  ++c->launches;
+  {
+    KClock k(c, kK_em_update);
+    CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+  }
   EmPassArgs p;
   p.y = r.tensor;
   p.segs = g.d_segs;
@@ -460,22 +506,32 @@ gss_status run_em(gss_b200_ctx* c, Group& g, const EmRun& r) {
   p.npat_max = g.npat_max;
   p.normalize = r.normalize;
   for (int it = 0; it < I; ++it) {
-    CU_TRY(c, launch_em_pass(shape, false, p, g.nwork, g.F, c->stream));
+    {
+      KClock k(c, kK_em_pass);
+      CU_TRY(c, launch_em_pass(shape, false, p, g.nwork, g.F, c->stream));
+    }
     u.mode = kEmMstep;
     u.bin_ll = g.bin_ll + (long long)it * g.nF;
-    CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
-    c->launches += 2;
+    {
+      KClock k(c, kK_em_update);
+      CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+    }
   }
   p.gamma = g.gamma;
-  CU_TRY(c, launch_em_pass(shape, r.final_stats, p, g.nwork, g.F, c->stream));
+  {
+    KClock k(c, kK_em_pass);
+    CU_TRY(c, launch_em_pass(shape, r.final_stats, p, g.nwork, g.F, c->stream));
+  }
   u.mode = kEmFinal;
   u.bin_ll = g.bin_ll + (long long)I * g.nF;
-  CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
-  c->launches += 2;
+  {
+    KClock k(c, kK_em_update);
+    CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+  }
   for (int it = r.all_ll ? 0 : I; it <= I; ++it) {
+    KClock k(c, kK_misc);
     CU_TRY(c, launch_sum_ll(g.bin_ll + (long long)it * g.nF, g.seg_ll + (long long)it * g.nseg, g.d_segs, g.nseg,
                             g.F, c->stream));
-    ++c->launches;
   }
   return GSS_OK;
 }
@@ -494,9 +550,14 @@ gss_status run_mvdr_design(gss_b200_ctx* c, Group& g, int fixed_ref, bool have_t
   a.M = g.M;
   a.F = g.F;
   a.fixed_ref = fixed_ref;
-  CU_TRY(c, launch_select_reference(a, g.nseg, c->stream));
-  CU_TRY(c, launch_mvdr_solve(a, g.nseg, c->stream));
-  c->launches += 2;
+  {
+    KClock k(c, kK_mvdr);
+    CU_TRY(c, launch_select_reference(a, g.nseg, c->stream));
+  }
+  {
+    KClock k(c, kK_mvdr);
+    CU_TRY(c, launch_mvdr_solve(a, g.nseg, c->stream));
+  }
   return GSS_OK;
 }
 
@@ -591,6 +652,8 @@ void gss_b200_destroy(gss_b200_ctx* c) {
   for (auto& kv : c->tables) {
     cudaFree(kv.second.tw);
     cudaFree(kv.second.win);
+    cudaFree(kv.second.tw_d);
+    cudaFree(kv.second.win_d);
   }
   cudaStreamDestroy(c->stream);
   delete c;
@@ -610,6 +673,65 @@ gss_status gss_b200_host_alloc(int64_t bytes, void** out) {
 }
 void gss_b200_host_free(void* p) {
   if (p) cudaFreeHost(p);
+}
+
+gss_status gss_b200_profile(gss_b200_ctx* c, int32_t enable) {
+  cudaStreamSynchronize(c->stream);
+  for (auto& r : c->prof_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  c->prof_recs.clear();
+  for (int i = 0; i < GSS_B200_NUM_KERNELS; ++i) {
+    c->kernel_ms[i] = 0.0;
+    c->kernel_launches[i] = 0;
+  }
+  c->prof_on = enable != 0;
+  return GSS_OK;
+}
+
+gss_status gss_b200_kernel_ms(gss_b200_ctx* c, double* ms, int64_t* launches) {
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  for (auto& r : c->prof_recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) c->kernel_ms[r.id] += t;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  c->prof_recs.clear();
+  for (int i = 0; i < GSS_B200_NUM_KERNELS; ++i) {
+    ms[i] = c->kernel_ms[i];
+    launches[i] = c->kernel_launches[i];
+  }
+  return GSS_OK;
+}
+
+gss_status gss_b200_fp32_peak(gss_b200_ctx* c, double* tflops) {
+  CU_TRY(c, cudaSetDevice(c->device));
+  float* scratch = nullptr;
+  CU_TRY(c, cudaMalloc(&scratch, 256));
+  cudaDeviceProp prop;
+  CU_TRY(c, cudaGetDeviceProperties(&prop, c->device));
+  const int ctas = prop.multiProcessorCount * 8, iters = 2048;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  double best = 0.0;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(a, c->stream);
+    cudaError_t e = launch_fma_peak(scratch, ctas, iters, c->stream);
+    cudaEventRecord(b, c->stream);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (e == cudaSuccess && rep > 0 && ms > 0.f)
+      best = std::max(best, 2.0 * 256.0 * iters * 256.0 * ctas / (ms * 1e-3) * 1e-12);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(scratch);
+  *tflops = best;
+  return GSS_OK;
 }
 
 gss_status gss_b200_stage_ms(gss_b200_ctx* c, double* ms) {
@@ -740,13 +862,14 @@ gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) {
       a.audio = g.audio;
       a.y = g.Y;
       a.segs = g.d_segs;
-      a.tw = b->tables.tw;
-      a.win = b->tables.win;
+      a.tw_d = b->tables.tw_d;
+      a.win_d = b->tables.win_d;
       a.p = sp;
       a.M = g.M;
       a.TB = 0;
+      a.fft_warps = 0;
+      KClock k(c, kK_stft);
       CU_TRY(c, launch_stft(a, g.nseg, g.max_T, st));
-      ++c->launches;
     }
     cudaEventRecord(ev[1], st);
     const float2* tensor = g.Y;
@@ -771,8 +894,10 @@ gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) {
       sf.tmass = g.tmass;
       sf.cell_stride = g.cell_stride;
       sf.F = g.F;
-      CU_TRY(c, launch_mvdr_stats_final(EmShape{g.M, g.KT}, sf, g.nseg, st));
-      ++c->launches;
+      {
+        KClock k(c, kK_mvdr);
+        CU_TRY(c, launch_mvdr_stats_final(EmShape{g.M, g.KT}, sf, g.nseg, st));
+      }
       gss_status rc = run_mvdr_design(c, g, -1, true);
       if (rc != GSS_OK) return rc;
       ApplyArgs aa;
@@ -783,8 +908,8 @@ gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) {
       aa.M = g.M;
       aa.F = g.F;
       aa.frame_major = 1;
+      KClock k(c, kK_apply);
       CU_TRY(c, launch_apply(aa, g.nseg, g.max_T, st));
-      ++c->launches;
     }
     cudaEventRecord(ev[4], st);
     {
@@ -796,8 +921,8 @@ gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) {
       ia.win = b->tables.win;
       ia.p = sp;
       ia.HB = 0;
+      KClock k(c, kK_istft);
       CU_TRY(c, launch_istft(ia, g.nseg, g.max_N, st));
-      ++c->launches;
     }
     cudaEventRecord(ev[5], st);
   }
@@ -999,13 +1124,16 @@ gss_status gss_b200_stft(gss_b200_ctx* c, const float* audio, int32_t M, int64_t
   a.audio = sg.g.audio;
   a.y = sg.g.Y;
   a.segs = sg.g.d_segs;
-  a.tw = tb.tw;
-  a.win = tb.win;
+  a.tw_d = tb.tw_d;
+  a.win_d = tb.win_d;
   a.p = stft_params(*cfg);
   a.M = M;
   a.TB = 0;
-  CU_TRY(c, launch_stft(a, 1, (int)T, c->stream));
-  ++c->launches;
+  a.fft_warps = 0;
+  {
+    KClock k(c, kK_stft);
+    CU_TRY(c, launch_stft(a, 1, (int)T, c->stream));
+  }
   CU_TRY(c, cudaMemcpyAsync(out, sg.g.Y, sizeof(float2) * (size_t)F * T * M, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   return GSS_OK;
@@ -1052,7 +1180,10 @@ gss_status gss_b200_istft(gss_b200_ctx* c, const float* spec, int32_t bins, int6
     aa.M = M;
     aa.F = F;
     aa.frame_major = 1;
-    CU_TRY(c, launch_apply(aa, 1, (int)T, c->stream));
+    {
+      KClock k(c, kK_apply);
+      CU_TRY(c, launch_apply(aa, 1, (int)T, c->stream));
+    }
     IstftArgs ia;
     ia.x = g.X;
     ia.wave = g.wave;
@@ -1061,8 +1192,10 @@ gss_status gss_b200_istft(gss_b200_ctx* c, const float* spec, int32_t bins, int6
     ia.win = tb.win;
     ia.p = stft_params(*cfg);
     ia.HB = 0;
-    CU_TRY(c, launch_istft(ia, 1, out_len, c->stream));
-    c->launches += 2;
+    {
+      KClock k(c, kK_istft);
+      CU_TRY(c, launch_istft(ia, 1, out_len, c->stream));
+    }
     CU_TRY(c, cudaMemcpyAsync(out + (size_t)ch * out_len, g.wave, sizeof(float) * out_len, cudaMemcpyDeviceToHost,
                               c->stream));
     CU_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1113,8 +1246,10 @@ gss_status gss_b200_unit_normalize(gss_b200_ctx* c, const float* in, int32_t bin
   if (rc != GSS_OK) return rc;
   const size_t bytes = sizeof(float2) * (size_t)bins * T * M;
   CU_TRY(c, cudaMemcpyAsync(sg.g.Y, in, bytes, cudaMemcpyHostToDevice, c->stream));
-  CU_TRY(c, launch_unit_normalize(sg.g.Y, sg.g.Yd, (long long)bins * T, M, c->stream));
-  ++c->launches;
+  {
+    KClock k(c, kK_misc);
+    CU_TRY(c, launch_unit_normalize(sg.g.Y, sg.g.Yd, (long long)bins * T, M, c->stream));
+  }
   CU_TRY(c, cudaMemcpyAsync(out, sg.g.Yd, bytes, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   return GSS_OK;
@@ -1228,7 +1363,10 @@ gss_status gss_b200_mvdr_stats(gss_b200_ctx* c, const float* y, const float* gam
   sp.work = g.d_work;
   sp.part = g.part;
   sp.cell_stride = g.cell_stride;
-  CU_TRY(c, launch_mvdr_stats(EmShape{g.M, g.KT}, sp, g.nwork, bins, c->stream));
+  {
+    KClock k(c, kK_mvdr);
+    CU_TRY(c, launch_mvdr_stats(EmShape{g.M, g.KT}, sp, g.nwork, bins, c->stream));
+  }
   StatsFinalArgs sf;
   sf.segs = g.d_segs;
   sf.part = g.part;
@@ -1237,8 +1375,10 @@ gss_status gss_b200_mvdr_stats(gss_b200_ctx* c, const float* y, const float* gam
   sf.tmass = g.tmass;
   sf.cell_stride = g.cell_stride;
   sf.F = bins;
-  CU_TRY(c, launch_mvdr_stats_final(EmShape{g.M, g.KT}, sf, 1, c->stream));
-  c->launches += 2;
+  {
+    KClock k(c, kK_mvdr);
+    CU_TRY(c, launch_mvdr_stats_final(EmShape{g.M, g.KT}, sf, 1, c->stream));
+  }
   std::vector<double> tm(bins);
   CU_TRY(c, cudaMemcpyAsync(tm.data(), g.tmass, sizeof(double) * bins, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaMemcpyAsync(tgt, g.phi_t, sizeof(cdbl) * (size_t)bins * M * M, cudaMemcpyDeviceToHost, c->stream));
@@ -1290,8 +1430,10 @@ static gss_status mvdr_common(gss_b200_ctx* c, const double* tgt, const double* 
     a.M = M;
     a.F = bins;
     a.fixed_ref = -1;
-    CU_TRY(c, launch_select_reference(a, 1, c->stream));
-    ++c->launches;
+    {
+      KClock k(c, kK_mvdr);
+      CU_TRY(c, launch_select_reference(a, 1, c->stream));
+    }
     int r = 0;
     CU_TRY(c, cudaMemcpyAsync(&r, g.ref, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CU_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1337,8 +1479,10 @@ gss_status gss_b200_apply(gss_b200_ctx* c, const double* h, int32_t h_bins, int3
   aa.M = M;
   aa.F = bins;
   aa.frame_major = 0;
-  CU_TRY(c, launch_apply(aa, 1, (int)T, c->stream));
-  ++c->launches;
+  {
+    KClock k(c, kK_apply);
+    CU_TRY(c, launch_apply(aa, 1, (int)T, c->stream));
+  }
   CU_TRY(c, cudaMemcpyAsync(out, g.X, sizeof(float2) * (size_t)bins * T, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   return GSS_OK;

@@ -112,6 +112,30 @@ __global__ void sum_ll_kernel(const double* bin_ll, double* out, const SegDev* s
   out[s] = ll;
 }
 
+// FP32 FMA calibration: 16 independent chains per thread, 4096 FMAs per chain step; the
+// denominator of the FP32-bound kernels' roofline fraction (bench harness only).
+__global__ void __launch_bounds__(256) fma_peak_kernel(float* out, int iters) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = (float)(threadIdx.x + i) * 1e-3f;
+  const float b = 0.999f, c = 1e-4f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = fmaf(a[i], b, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i];
+  if (s == 123.456f) out[0] = s;
+}
+
+cudaError_t launch_fma_peak(float* scratch, int ctas, int iters, cudaStream_t st) {
+  fma_peak_kernel<<<ctas, 256, 0, st>>>(scratch, iters);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select_reference(const MvdrArgs& a, int nseg, cudaStream_t st) {
   select_reference_kernel<<<nseg, 32, 0, st>>>(a);
   return cudaGetLastError();

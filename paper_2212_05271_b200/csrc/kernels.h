@@ -10,10 +10,10 @@ struct StftArgs {
   const float* audio;
   float2* y;
   const SegDev* segs;
-  const float2* tw;   // exp(-2 pi i k / n), k < n/2
-  const float* win;   // analysis window, n floats
+  const double2* tw_d;  // exp(-2 pi i k / n), k < n/2
+  const double* win_d;  // analysis window, n doubles
   StftParams p;
-  int M, TB;
+  int M, TB, fft_warps;
 };
 struct ApplyArgs {
   const float2* y;
@@ -50,9 +50,9 @@ struct WpeArgs {
   int M, taps, delay, psd_context;
 };
 int wpe_gram_tiles(int km);
-/// power -> gram -> solve -> apply (4 launches)
-cudaError_t launch_wpe_iteration(const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
-                                 cudaStream_t st, long long* launches);
+/// one kernel of a WPE iteration; step: 0 power, 1 gram, 2 solve, 3 apply
+cudaError_t launch_wpe_step(int step, const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
+                            cudaStream_t st);
 
 // ---- cACGMM EM + MVDR statistics (cacgmm_kernels.cuh, cacgmm_m*.cu) -----------
 enum EmUpdateMode { kEmInit = 0, kEmMstep = 1, kEmFinal = 2, kEmFromState = 3 };
@@ -148,6 +148,8 @@ struct MvdrArgs {
 cudaError_t launch_select_reference(const MvdrArgs& a, int nseg, cudaStream_t st);
 cudaError_t launch_mvdr_solve(const MvdrArgs& a, int nseg, cudaStream_t st);
 cudaError_t launch_unit_normalize(const float2* in, float2* out, long long frames_total, int M, cudaStream_t st);
+/// 256 * iters FMAs per thread, 256 threads per CTA
+cudaError_t launch_fma_peak(float* scratch, int ctas, int iters, cudaStream_t st);
 cudaError_t launch_sum_ll(const double* bin_ll, double* out, const SegDev* segs, int nseg, int F, cudaStream_t st);
 
 }  // namespace gssb

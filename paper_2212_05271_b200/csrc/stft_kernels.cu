@@ -8,6 +8,8 @@
 // FFTs: one warp transforms one complex sequence of n points in shared memory
 // (radix-2 decimation in time). Two real sequences ride in one complex
 // transform (x1 + i x2), which halves the work of the real transforms.
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace gssb {
@@ -19,9 +21,8 @@ constexpr int kStftWarps = kStftThreads / 32;
 
 /// In-place radix-2 DIT over bit-reversed input; tw[k] = exp(-2 pi i k / n).
 /// INVERSE conjugates the twiddles (unscaled inverse).
-template <bool INVERSE>
-__device__ __forceinline__ void warp_fft(float2* buf, const float2* __restrict__ tw, int n, int log2n,
-                                         int lane) {
+template <bool INVERSE, typename C2>
+__device__ __forceinline__ void warp_fft(C2* buf, const C2* __restrict__ tw, int n, int log2n, int lane) {
   for (int s = 1; s <= log2n; ++s) {
     const int half = 1 << (s - 1);
     const int tstep = n >> s;
@@ -29,12 +30,18 @@ __device__ __forceinline__ void warp_fft(float2* buf, const float2* __restrict__
       const int pos = b & (half - 1);
       const int i0 = ((b >> (s - 1)) << s) + pos;
       const int i1 = i0 + half;
-      float2 w = tw[pos * tstep];
+      C2 w = tw[pos * tstep];
       if (INVERSE) w.y = -w.y;
-      const float2 u = buf[i0], x = buf[i1];
-      const float2 v = make_float2(x.x * w.x - x.y * w.y, x.x * w.y + x.y * w.x);
-      buf[i0] = make_float2(u.x + v.x, u.y + v.y);
-      buf[i1] = make_float2(u.x - v.x, u.y - v.y);
+      const C2 u = buf[i0], x = buf[i1];
+      C2 v, r0, r1;
+      v.x = x.x * w.x - x.y * w.y;
+      v.y = x.x * w.y + x.y * w.x;
+      r0.x = u.x + v.x;
+      r0.y = u.y + v.y;
+      r1.x = u.x - v.x;
+      r1.y = u.y - v.y;
+      buf[i0] = r0;
+      buf[i1] = r1;
     }
     __syncwarp();
   }
@@ -62,10 +69,14 @@ __device__ __forceinline__ long long reflect_index(long long idx, long long N) {
 // runs of TB*M contiguous cfloats per bin (the (F,T,M) layout of stft.hpp:52-80).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kStftThreads) stft_kernel(StftArgs a) {
+  // The forward transform runs in FP64 like the reference's (stft.hpp:158-170,
+  // double FFT then a cast to cfloat): an FP32 FFT leaves an error proportional
+  // to the frame's LOUDEST bin in every bin, which the EM iterations amplify in
+  // the quiet bins.
   extern __shared__ float4 smem_f4[];
-  float2* fftbuf = reinterpret_cast<float2*>(smem_f4);
-  const int n = a.p.fft_size, log2n = a.p.log2n, F = a.p.F, M = a.M, TB = a.TB;
-  float2* tile = fftbuf + kStftWarps * n;
+  double2* fftbuf = reinterpret_cast<double2*>(smem_f4);
+  const int n = a.p.fft_size, log2n = a.p.log2n, F = a.p.F, M = a.M, TB = a.TB, NFW = a.fft_warps;
+  float2* tile = reinterpret_cast<float2*>(fftbuf + NFW * n);
   const int run = TB * M;
   const int pitch = run | 1;
   const SegDev sd = a.segs[blockIdx.y];
@@ -74,9 +85,9 @@ __global__ void __launch_bounds__(kStftThreads) stft_kernel(StftArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pad = n / 2;
   const long long N = sd.N;
-  float2* buf = fftbuf + warp * n;
+  double2* buf = fftbuf + (warp < NFW ? warp : 0) * n;
   const int npairs = (run + 1) / 2;
-  for (int pair = warp; pair < npairs; pair += kStftWarps) {
+  for (int pair = warp; pair < npairs && warp < NFW; pair += NFW) {
     const int s1 = 2 * pair, s2 = s1 + 1;
     const int tl1 = s1 / M, m1 = s1 % M, tl2 = s2 / M, m2 = s2 % M;
     const bool v1 = t0 + tl1 < sd.T;
@@ -86,17 +97,17 @@ __global__ void __launch_bounds__(kStftThreads) stft_kernel(StftArgs a) {
     const long long b1 = (long long)(t0 + tl1) * a.p.shift - pad;
     const long long b2 = (long long)(t0 + tl2) * a.p.shift - pad;
     for (int i = lane; i < n; i += 32) {
-      const float w = a.win[i];
-      const float r1 = v1 ? x1[reflect_index(b1 + i, N)] * w : 0.f;
-      const float r2 = v2 ? x2[reflect_index(b2 + i, N)] * w : 0.f;
-      buf[__brev((unsigned)i) >> (32 - log2n)] = make_float2(r1, r2);
+      const double w = a.win_d[i];
+      const double r1 = v1 ? (double)x1[reflect_index(b1 + i, N)] * w : 0.0;
+      const double r2 = v2 ? (double)x2[reflect_index(b2 + i, N)] * w : 0.0;
+      buf[__brev((unsigned)i) >> (32 - log2n)] = make_double2(r1, r2);
     }
     __syncwarp();
-    warp_fft<false>(buf, a.tw, n, log2n, lane);
+    warp_fft<false>(buf, a.tw_d, n, log2n, lane);
     for (int f = lane; f <= n / 2; f += 32) {
-      const float2 zf = buf[f], zn = buf[(n - f) & (n - 1)];
-      if (v1) tile[f * pitch + s1] = make_float2(0.5f * (zf.x + zn.x), 0.5f * (zf.y - zn.y));
-      if (v2) tile[f * pitch + s2] = make_float2(0.5f * (zf.y + zn.y), 0.5f * (zn.x - zf.x));
+      const double2 zf = buf[f], zn = buf[(n - f) & (n - 1)];
+      if (v1) tile[f * pitch + s1] = make_float2((float)(0.5 * (zf.x + zn.x)), (float)(0.5 * (zf.y - zn.y)));
+      if (v2) tile[f * pitch + s2] = make_float2((float)(0.5 * (zf.y + zn.y)), (float)(0.5 * (zn.x - zf.x)));
     }
     __syncwarp();
   }
@@ -220,13 +231,15 @@ __global__ void __launch_bounds__(kStftThreads) istft_kernel(IstftArgs a) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-static int stft_frames_per_cta(int n) { return n >= 4096 ? 1 : 4096 / n; }
+static int stft_frames_per_cta(int n) { return n <= 512 ? 4096 / n : (n >= 2048 ? 1 : 2048 / n); }
+static int stft_fft_warps(int n) { return std::max(1, std::min(kStftWarps, 8192 / n)); }
 
 cudaError_t launch_stft(const StftArgs& args_in, int nseg, int max_frames, cudaStream_t st) {
   StftArgs a = args_in;
   a.TB = stft_frames_per_cta(a.p.fft_size);
-  const size_t smem =
-      sizeof(float2) * ((size_t)kStftWarps * a.p.fft_size + (size_t)a.p.F * ((a.TB * a.M) | 1));
+  a.fft_warps = stft_fft_warps(a.p.fft_size);
+  const size_t smem = sizeof(double2) * (size_t)a.fft_warps * a.p.fft_size +
+                      sizeof(float2) * (size_t)a.p.F * ((a.TB * a.M) | 1);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(stft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -370,15 +370,13 @@ __global__ void __launch_bounds__(256) wpe_apply_kernel(WpeArgs a) {
 int wpe_gram_tiles(int km) { return gram_num_tiles(km); }
 
 template <int M>
-static cudaError_t launch_wpe_iter_m(const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
-                                     cudaStream_t st, long long* launches) {
+static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
+                                     cudaStream_t st) {
   const int km = a.taps * M, H = a.delay + a.taps - 1;
-  {
+  if (step == 0) {
     dim3 grid((max_frames + 255) / 256, F, nseg);
     wpe_power_kernel<<<grid, 256, 0, st>>>(a);
-    ++*launches;
-  }
-  {
+  } else if (step == 1) {
     const int ngroups = (gram_num_tiles(km) + kGramWarps - 1) / kGramWarps;
     const size_t smem = sizeof(float2) * (size_t)M * ((kGramTileFrames + H) | 1) + sizeof(float) * kGramTileFrames;
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
@@ -386,40 +384,36 @@ static cudaError_t launch_wpe_iter_m(const WpeArgs& a, int nseg, int F, int max_
     if (e != cudaSuccess) return e;
     dim3 grid(ngroups * max_wchunks, F, nseg);
     wpe_gram_kernel<M><<<grid, kGramThreads, smem, st>>>(a);
-    ++*launches;
-  }
-  {
+  } else if (step == 2) {
     const size_t smem = sizeof(cdbl) * ((size_t)km * (km + 1) + (size_t)km * M);
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(wpe_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(F, nseg);
     wpe_solve_kernel<<<grid, 256, smem, st>>>(a);
-    ++*launches;
-  }
-  {
+  } else {
     const size_t smem = sizeof(float2) * ((size_t)M * ((256 + H) | 1) + (size_t)km * M);
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(wpe_apply_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((max_frames + 255) / 256, F, nseg);
     wpe_apply_kernel<M><<<grid, 256, smem, st>>>(a);
-    ++*launches;
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_wpe_iteration(const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
-                                 cudaStream_t st, long long* launches) {
+/// step: 0 power, 1 gram, 2 solve, 3 apply
+cudaError_t launch_wpe_step(int step, const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
+                            cudaStream_t st) {
   switch (a.M) {
-    case 1: return launch_wpe_iter_m<1>(a, nseg, F, max_frames, max_wchunks, st, launches);
-    case 2: return launch_wpe_iter_m<2>(a, nseg, F, max_frames, max_wchunks, st, launches);
-    case 3: return launch_wpe_iter_m<3>(a, nseg, F, max_frames, max_wchunks, st, launches);
-    case 4: return launch_wpe_iter_m<4>(a, nseg, F, max_frames, max_wchunks, st, launches);
-    case 5: return launch_wpe_iter_m<5>(a, nseg, F, max_frames, max_wchunks, st, launches);
-    case 6: return launch_wpe_iter_m<6>(a, nseg, F, max_frames, max_wchunks, st, launches);
-    case 7: return launch_wpe_iter_m<7>(a, nseg, F, max_frames, max_wchunks, st, launches);
-    case 8: return launch_wpe_iter_m<8>(a, nseg, F, max_frames, max_wchunks, st, launches);
+    case 1: return launch_wpe_step_m<1>(step, a, nseg, F, max_frames, max_wchunks, st);
+    case 2: return launch_wpe_step_m<2>(step, a, nseg, F, max_frames, max_wchunks, st);
+    case 3: return launch_wpe_step_m<3>(step, a, nseg, F, max_frames, max_wchunks, st);
+    case 4: return launch_wpe_step_m<4>(step, a, nseg, F, max_frames, max_wchunks, st);
+    case 5: return launch_wpe_step_m<5>(step, a, nseg, F, max_frames, max_wchunks, st);
+    case 6: return launch_wpe_step_m<6>(step, a, nseg, F, max_frames, max_wchunks, st);
+    case 7: return launch_wpe_step_m<7>(step, a, nseg, F, max_frames, max_wchunks, st);
+    case 8: return launch_wpe_step_m<8>(step, a, nseg, F, max_frames, max_wchunks, st);
     default: return cudaErrorInvalidValue;
   }
 }

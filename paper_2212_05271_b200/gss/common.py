@@ -41,6 +41,22 @@ class Context:
         self.check(self.lib.gss_b200_stage_ms(self.handle, ms))
         return dict(zip(capi.STAGE_NAMES, [float(v) for v in ms]))
 
+    def profile(self, enable: bool = True):
+        """Reset and (de)activate the per-kernel CUDA-event clocks."""
+        self.check(self.lib.gss_b200_profile(self.handle, C.c_int32(1 if enable else 0)))
+
+    def kernel_ms(self) -> dict:
+        """{kernel class: (summed device ms, launches)} since the last profile() call."""
+        ms = (C.c_double * capi.NUM_KERNELS)()
+        n = (C.c_int64 * capi.NUM_KERNELS)()
+        self.check(self.lib.gss_b200_kernel_ms(self.handle, ms, n))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(capi.KERNEL_NAMES)}
+
+    def fp32_peak_tflops(self) -> float:
+        v = C.c_double()
+        self.check(self.lib.gss_b200_fp32_peak(self.handle, C.byref(v)))
+        return v.value
+
     def close(self):
         if self.handle is not None:
             self.lib.gss_b200_destroy(self.handle)
