@@ -111,18 +111,33 @@ __device__ __forceinline__ void cp_async_wait() {
 //   FINAL = false: accumulators are the KT M-step Grams (weights gamma/q).
 //   FINAL = true : accumulators are the MVDR target / background Grams.
 // ---------------------------------------------------------------------------
+/// B^-1 coefficients live in shared memory ([lane g][class][NDOFP], NDOFP = NDOF rounded up to 4 so a
+/// lane fetches them as float4); that keeps the register tile to the accumulators and lets two CTAs
+/// share an SM when the accumulators are small enough.
 template <int M, int L, int KT, bool FINAL>
-__global__ void __launch_bounds__(kEmThreads, 1) em_pass_kernel(EmPassArgs a) {
+struct EmPassCfg {
+  static constexpr int NDOF = EmLayout<M, L>::NDOF;
+  static constexpr int NDOFP = (NDOF + 3) & ~3;
+  static constexpr int NA = FINAL ? 2 : KT;
+  static constexpr int MINB = (NA * NDOF <= 64) ? 2 : 1;
+  static constexpr int COEF_FLOATS = L * KT * NDOFP;
+};
+
+template <int M, int L, int KT, bool FINAL>
+__global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) em_pass_kernel(EmPassArgs a) {
   using Lay = EmLayout<M, L>;
+  using Cfg = EmPassCfg<M, L, KT, FINAL>;
   constexpr int NA = FINAL ? 2 : KT;
   using PL = PartLayout<M, L, KT, NA>;
   constexpr int NDOF = Lay::NDOF;
+  constexpr int NDOFP = Cfg::NDOFP;
   constexpr int SLOTS = kEmThreads / L;
   constexpr int TILE = kEmTileFrames;
   constexpr int NW = kEmThreads / 32;
   extern __shared__ float4 smem_f4[];
   float2* slab = reinterpret_cast<float2*>(smem_f4);                 // 2 * TILE * M
-  float* s_ck = reinterpret_cast<float*>(slab + 2 * TILE * M);       // npat_max * KT
+  float* s_coef = reinterpret_cast<float*>(slab + 2 * TILE * M);     // L * KT * NDOFP (16-byte aligned)
+  float* s_ck = s_coef + Cfg::COEF_FLOATS;                           // npat_max * KT
   unsigned char* s_pat = reinterpret_cast<unsigned char*>(s_ck + a.npat_max * KT);  // 2 * TILE
 
   const int tid = threadIdx.x;
@@ -151,14 +166,14 @@ __global__ void __launch_bounds__(kEmThreads, 1) em_pass_kernel(EmPassArgs a) {
   }
 
   const int g = tid % L, slot = tid / L;
-  float coef[KT][NDOF];
   {
-    const float* cp = a.coef + sd.coef_off + ((long long)f * L + g) * (KT * NDOF);
-#pragma unroll
-    for (int k = 0; k < KT; ++k)
-#pragma unroll
-      for (int j = 0; j < NDOF; ++j) coef[k][j] = cp[k * NDOF + j];
+    const float* cp = a.coef + sd.coef_off + (long long)f * L * (KT * NDOF);
+    for (int i = tid; i < L * KT * NDOFP; i += kEmThreads) {
+      const int j = i % NDOFP, gk = i / NDOFP;
+      s_coef[i] = j < NDOF ? cp[gk * NDOF + j] : 0.f;
+    }
   }
+  const float4* c4 = reinterpret_cast<const float4*>(s_coef + g * KT * NDOFP);
   float acc[NA][NDOF];
   float mass[KT];
 #pragma unroll
@@ -212,12 +227,17 @@ __global__ void __launch_bounds__(kEmThreads, 1) em_pass_kernel(EmPassArgs a) {
       }
       float q[KT];
 #pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        float s = 0.f;
+      for (int k = 0; k < KT; ++k) q[k] = 0.f;
 #pragma unroll
-        for (int j = 0; j < NDOF; ++j) s = fmaf(coef[k][j], pv[j], s);
-        q[k] = s;
-      }
+      for (int j4 = 0; j4 < NDOFP / 4; ++j4)
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          const float4 c = c4[k * (NDOFP / 4) + j4];
+          q[k] = fmaf(c.x, pv[4 * j4], q[k]);
+          if (4 * j4 + 1 < NDOF) q[k] = fmaf(c.y, pv[4 * j4 + 1 < NDOF ? 4 * j4 + 1 : 0], q[k]);
+          if (4 * j4 + 2 < NDOF) q[k] = fmaf(c.z, pv[4 * j4 + 2 < NDOF ? 4 * j4 + 2 : 0], q[k]);
+          if (4 * j4 + 3 < NDOF) q[k] = fmaf(c.w, pv[4 * j4 + 3 < NDOF ? 4 * j4 + 3 : 0], q[k]);
+        }
 #pragma unroll
       for (int o = 1; o < L; o <<= 1)
 #pragma unroll
