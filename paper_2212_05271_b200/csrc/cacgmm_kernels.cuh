@@ -25,6 +25,24 @@
 
 namespace gssb {
 
+/// How the 32 lanes of a warp map to (frame slot, lane-in-frame g) and the shared-memory frame stride
+/// (float2 units), chosen by brute force over the bank model so that the per-lane frame loads of
+/// FramePlan::dofs are (nearly) conflict free:
+///   SPREAD (L <= 4): g = lane / (32/L), slot = lane % (32/L)  -- the L lanes of a frame are 32/L apart
+///   else           : g = lane % L,      slot = lane / L
+template <int M, int L>
+struct LaneMap {
+  static constexpr bool SPREAD = L <= 4;
+  static constexpr int SPW = 32 / L;  // frame slots per warp
+  static constexpr int STRIDE = !SPREAD ? M : (M == 7 ? 10 : M == 8 ? 10 : M == 4 ? 5 : M == 2 ? 3 : M);
+  __device__ static __forceinline__ int g_of(int lane) { return SPREAD ? lane / SPW : lane % L; }
+  __device__ static __forceinline__ int slot_of(int lane) { return SPREAD ? lane % SPW : lane / L; }
+  /// xor offsets that stay inside a frame's lane group / that walk over the slots of a warp
+  static constexpr int G_LO = SPREAD ? SPW : 1, G_HI = SPREAD ? 32 : L;
+  static constexpr int S_LO = SPREAD ? 1 : L, S_HI = SPREAD ? SPW : 32;
+  __device__ static __forceinline__ int lane_of_g(int g) { return SPREAD ? g * SPW : g; }
+};
+
 // ---------------------------------------------------------------------------
 // Per-lane view of one frame
 // ---------------------------------------------------------------------------
@@ -78,7 +96,7 @@ struct FramePlan {
 #pragma unroll
     for (int i = 0; i < Lay::RPL; ++i) s = fmaf(rowmask[i], pv[i * M], s);
 #pragma unroll
-    for (int o = 1; o < L; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    for (int o = LaneMap<M, L>::G_LO; o < LaneMap<M, L>::G_HI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     return s;
   }
 };
@@ -120,7 +138,9 @@ struct EmPassCfg {
   static constexpr int NDOFP = (NDOF + 3) & ~3;
   static constexpr int NA = FINAL ? 2 : KT;
   static constexpr int MINB = (NA * NDOF <= 64) ? 2 : 1;
-  static constexpr int COEF_FLOATS = L * KT * NDOFP;
+  static constexpr int COEF_G = KT * NDOFP + 4;  // per-lane-group stride, skewed by one float4 against bank conflicts
+  static constexpr int COEF_FLOATS = L * COEF_G;
+  static constexpr int FS = LaneMap<M, L>::STRIDE;  // frame stride in the pipeline buffers
 };
 
 template <int M, int L, int KT, bool FINAL>
@@ -135,8 +155,10 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
   constexpr int TILE = kEmTileFrames;
   constexpr int NW = kEmThreads / 32;
   extern __shared__ float4 smem_f4[];
-  float2* slab = reinterpret_cast<float2*>(smem_f4);                 // 2 * TILE * M
-  float* s_coef = reinterpret_cast<float*>(slab + 2 * TILE * M);     // L * KT * NDOFP (16-byte aligned)
+  using LM = LaneMap<M, L>;
+  constexpr int FS = Cfg::FS;
+  float2* slab = reinterpret_cast<float2*>(smem_f4);                 // 2 * TILE * FS
+  float* s_coef = reinterpret_cast<float*>(slab + 2 * TILE * FS);    // COEF_FLOATS (16-byte aligned)
   float* s_ck = s_coef + Cfg::COEF_FLOATS;                           // npat_max * KT
   unsigned char* s_pat = reinterpret_cast<unsigned char*>(s_ck + a.npat_max * KT);  // 2 * TILE
 
@@ -153,8 +175,8 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
   auto issue_tile = [&](int tile, int buf) {
     const int n = min(TILE, nt - tile * TILE) * M;
     const float2* s = src + (long long)tile * TILE * M;
-    float2* d = slab + buf * TILE * M;
-    for (int i = tid; i < n; i += kEmThreads) cp_async8(d + i, s + i);
+    float2* d = slab + buf * TILE * FS;
+    for (int i = tid; i < n; i += kEmThreads) cp_async8(d + (FS == M ? i : (i / M) * FS + i % M), s + i);
     cp_async_commit();
   };
 
@@ -165,15 +187,16 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
     for (int i = tid; i < min(TILE, nt); i += kEmThreads) s_pat[i] = psrc[i];
   }
 
-  const int g = tid % L, slot = tid / L;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = LM::g_of(lane), slot = warp * LM::SPW + LM::slot_of(lane);
   {
     const float* cp = a.coef + sd.coef_off + (long long)f * L * (KT * NDOF);
     for (int i = tid; i < L * KT * NDOFP; i += kEmThreads) {
       const int j = i % NDOFP, gk = i / NDOFP;
-      s_coef[i] = j < NDOF ? cp[gk * NDOF + j] : 0.f;
+      s_coef[(gk / KT) * Cfg::COEF_G + (gk % KT) * NDOFP + j] = j < NDOF ? cp[gk * NDOF + j] : 0.f;
     }
   }
-  const float4* c4 = reinterpret_cast<const float4*>(s_coef + g * KT * NDOFP);
+  const float4* c4 = reinterpret_cast<const float4*>(s_coef + g * Cfg::COEF_G);
   float acc[NA][NDOF];
   float mass[KT];
 #pragma unroll
@@ -210,7 +233,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
     }
     __syncthreads();
     const int nin = min(TILE, nt - tile * TILE);
-    const float2* sl = slab + buf * TILE * M;
+    const float2* sl = slab + buf * TILE * FS;
     const unsigned char* sp = s_pat + buf * TILE;
 #pragma unroll 1
     for (int fb = slot; fb < TILE; fb += SLOTS) {
@@ -218,7 +241,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
       const bool valid = fb < nin;
       const int fbc = valid ? fb : nin - 1;
       float pv[NDOF];
-      plan.dofs(sl + fbc * M, pv);
+      plan.dofs(sl + fbc * FS, pv);
       float inv2 = 1.f;
       if (normalize) {
         const float nr = __fsqrt_rn(plan.norm2(pv)) + 1e-10f;  // wpe.hpp:135
@@ -239,7 +262,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
           if (4 * j4 + 3 < NDOF) q[k] = fmaf(c.w, pv[4 * j4 + 3 < NDOF ? 4 * j4 + 3 : 0], q[k]);
         }
 #pragma unroll
-      for (int o = 1; o < L; o <<= 1)
+      for (int o = LM::G_LO; o < LM::G_HI; o <<= 1)
 #pragma unroll
         for (int k = 0; k < KT; ++k) q[k] += __shfl_xor_sync(0xffffffffu, q[k], o);
 
@@ -299,7 +322,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
   // ---- reduce: frame slots within the warp, then warps through shared memory
   if (g != 0) ll = 0.0;
 #pragma unroll
-  for (int o = L; o < 32; o <<= 1) {
+  for (int o = LM::S_LO; o < LM::S_HI; o <<= 1) {
 #pragma unroll
     for (int k = 0; k < KT; ++k) mass[k] += __shfl_xor_sync(0xffffffffu, mass[k], o);
 #pragma unroll
@@ -312,9 +335,8 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
   __syncthreads();  // pipeline buffers are free
   float* red = reinterpret_cast<float*>(smem_f4);
   double* redll = reinterpret_cast<double*>(red + NW * PL::CELL + (NW * PL::CELL & 1));
-  const int lane = tid & 31, warp = tid >> 5;
-  if (lane < L) {
-    float* r = red + (warp * L + lane) * PL::STRIDE;
+  if (LM::slot_of(lane) == 0) {
+    float* r = red + (warp * L + g) * PL::STRIDE;
 #pragma unroll
     for (int n = 0; n < NA; ++n)
 #pragma unroll

@@ -25,7 +25,7 @@ namespace gssb {
 
 namespace {
 
-constexpr int kGramWarps = 8;
+constexpr int kGramWarps = 9;  // 54 tiles at M = 7 are 6 full groups; 204 registers x 288 threads fit one SM
 constexpr int kGramThreads = kGramWarps * 32;
 constexpr int kGramTileFrames = 512;  // frames staged per shared-memory tile
 
@@ -48,6 +48,15 @@ __device__ __forceinline__ void gram_tile_coords(int tile, int nb, int& bi, int&
   while ((r + 1) * (r + 2) / 2 <= tile) ++r;
   bi = r;
   bj = tile - r * (r + 1) / 2;
+}
+
+__device__ __forceinline__ void cp_async_bytes8(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_bytes4(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
 
 }  // namespace
@@ -84,7 +93,7 @@ __global__ void __launch_bounds__(256) wpe_power_kernel(WpeArgs a) {
 // Shared slab: [channel][frame] (pitch odd) so a warp's loads are contiguous.
 // ---------------------------------------------------------------------------
 template <int M>
-__global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
+__global__ void __maxnreg__(224) wpe_gram_kernel(WpeArgs a) {
   extern __shared__ float4 smem_f4[];
   const SegDev sd = a.segs[blockIdx.z];
   if (!sd.wpe_active) return;
@@ -96,8 +105,8 @@ __global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
   const int H = a.delay + a.taps - 1;
   const int SF = kGramTileFrames + H;      // slab frames per tile (history halo first)
   const int pitch = SF | 1;
-  float2* slab = reinterpret_cast<float2*>(smem_f4);          // M * pitch
-  float* wsm = reinterpret_cast<float*>(slab + M * pitch);     // kGramTileFrames
+  const int buf_floats = 2 * M * pitch + kGramTileFrames;       // one pipeline stage: slab + weights
+  float* stage0 = reinterpret_cast<float*>(smem_f4);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = group * kGramWarps + warp;
@@ -127,17 +136,40 @@ __global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
   const int t_begin = chunk * sd.WTC, t_end = min(sd.T, t_begin + sd.WTC);
   const float2* yf = a.yobs + sd.y_off + (long long)f * sd.T * M;
   const float* wf = a.w + sd.w_off + (long long)f * sd.T;
-  for (int tb = t_begin; tb < t_end; tb += kGramTileFrames) {
+  const int ntl = (t_end - t_begin + kGramTileFrames - 1) / kGramTileFrames;
+
+  // stage frames [tb-H, tb+nfr) channel-major (a transposing cp.async per element);
+  // frames < 0 are zero (wpe.hpp:74-75)
+  auto issue = [&](int tl, int buf) {
+    const int tb = t_begin + tl * kGramTileFrames;
     const int nfr = min(kGramTileFrames, t_end - tb);
-    __syncthreads();
-    // stage frames [tb-H, tb+nfr) channel-major; frames < 0 are zero (wpe.hpp:74-75)
+    float2* slab = reinterpret_cast<float2*>(stage0 + buf * buf_floats);
+    float* wsm = stage0 + buf * buf_floats + 2 * M * pitch;
     for (int i = tid; i < (nfr + H) * M; i += kGramThreads) {
       const int fr = i / M, c = i - fr * M;
       const int t = tb - H + fr;
-      slab[c * pitch + fr] = t >= 0 ? yf[(long long)t * M + c] : make_float2(0.f, 0.f);
+      if (t >= 0)
+        cp_async_bytes8(slab + c * pitch + fr, yf + (long long)t * M + c);
+      else
+        slab[c * pitch + fr] = make_float2(0.f, 0.f);
     }
-    for (int i = tid; i < nfr; i += kGramThreads) wsm[i] = wf[tb + i];
+    for (int i = tid; i < nfr; i += kGramThreads) cp_async_bytes4(wsm + i, wf + tb + i);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  issue(0, 0);
+  for (int tl = 0; tl < ntl; ++tl) {
+    const int buf = tl & 1;
+    if (tl + 1 < ntl) {
+      issue(tl + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncthreads();
+    const int nfr = min(kGramTileFrames, t_end - (t_begin + tl * kGramTileFrames));
+    const float2* slab = reinterpret_cast<const float2*>(stage0 + buf * buf_floats);
+    const float* wsm = stage0 + buf * buf_floats + 2 * M * pitch;
     if (live) {
       for (int fi = lane; fi < nfr; fi += 32) {
         const float w = wsm[fi];
@@ -161,6 +193,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
           }
       }
     }
+    __syncthreads();  // everyone is done with `buf` before the next iteration refills it
   }
   if (!live) return;
 #pragma unroll
@@ -378,7 +411,7 @@ static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F
     wpe_power_kernel<<<grid, 256, 0, st>>>(a);
   } else if (step == 1) {
     const int ngroups = (gram_num_tiles(km) + kGramWarps - 1) / kGramWarps;
-    const size_t smem = sizeof(float2) * (size_t)M * ((kGramTileFrames + H) | 1) + sizeof(float) * kGramTileFrames;
+    const size_t smem = 2 * (sizeof(float2) * (size_t)M * ((kGramTileFrames + H) | 1) + sizeof(float) * kGramTileFrames);
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(wpe_gram_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
