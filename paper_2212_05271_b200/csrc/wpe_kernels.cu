@@ -25,7 +25,7 @@ namespace gssb {
 
 namespace {
 
-constexpr int kGramWarps = 9;  // 54 tiles at M = 7 are 6 full groups; 204 registers x 288 threads fit one SM
+constexpr int kGramWarps = 8;
 constexpr int kGramThreads = kGramWarps * 32;
 constexpr int kGramTileFrames = 512;  // frames staged per shared-memory tile
 
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) wpe_power_kernel(WpeArgs a) {
 // Shared slab: [channel][frame] (pitch odd) so a warp's loads are contiguous.
 // ---------------------------------------------------------------------------
 template <int M>
-__global__ void __maxnreg__(224) wpe_gram_kernel(WpeArgs a) {
+__global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
   extern __shared__ float4 smem_f4[];
   const SegDev sd = a.segs[blockIdx.z];
   if (!sd.wpe_active) return;

@@ -1,0 +1,99 @@
+"""Multi-process (gloo, world size 2, CPU) test of the segment sharding + ordered host gather that the N > 1
+path uses. The enhancement function is a stand-in (no GPU here); the sharding logic is what is under test."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2212_05271_b200 import sharding
+
+
+class _Audio:
+    def __init__(self, m, n):
+        self.m, self.n = m, n
+
+    def num_channels(self):
+        return self.m
+
+
+class _Act:
+    def __init__(self, t, k):
+        self.frames, self.k = t, k
+
+    def num_classes(self):
+        return self.k
+
+
+class _Seg:
+    def __init__(self, i, m, t, k):
+        self.index, self.audio, self.activity = i, _Audio(m, t * 128), _Act(t, k)
+
+
+class _Wpe:
+    taps, iterations = 10, 3
+
+
+class _Cfg:
+    bss_iterations, enable_wpe, wpe = 20, True, _Wpe()
+
+
+def _segments():
+    rng = np.random.RandomState(0)
+    return [_Seg(i, int(rng.randint(2, 9)), int(rng.randint(500, 7000)), int(rng.randint(2, 6))) for i in range(23)]
+
+
+def test_shard_is_balanced_and_deterministic():
+    segs = _segments()
+    costs = [sharding.segment_cost(s.activity.frames, s.audio.m, s.activity.k, 20, 10, 3) for s in segs]
+    for world in (1, 2, 4, 8):
+        owned = sharding.shard(costs, world)
+        assert sorted(i for o in owned for i in o) == list(range(len(segs)))
+        assert owned == sharding.shard(costs, world)
+        loads = [sum(costs[i] for i in o) for o in owned]
+        assert max(loads) <= sum(costs) / world + max(costs)  # LPT bound
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    segs = _segments()
+    calls = []
+
+    def fake_enhance(batch, cfg):
+        calls.append([s.index for s in batch])
+        return [("enhanced", s.index, rank) for s in batch]
+
+    out = sharding.enhance_sharded(segs, _Cfg(), fake_enhance, rank, world)
+    q.put((rank, out, calls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_gather_is_ordered():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict()
+    for _ in range(2):
+        rank, out, calls = q.get(timeout=120)
+        got[rank] = (out, calls)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out0, calls0 = got[0]
+    out1, calls1 = got[1]
+    assert out1 is None
+    assert [o[1] for o in out0] == list(range(23))          # plan order restored on rank 0
+    owners = {o[1]: o[2] for o in out0}
+    assert sorted(calls0[0] + calls1[0]) == list(range(23))  # every segment enhanced exactly once
+    assert all(owners[i] == 0 for i in calls0[0]) and all(owners[i] == 1 for i in calls1[0])
