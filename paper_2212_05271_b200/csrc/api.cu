@@ -282,7 +282,7 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
   g.cell_stride = em_cell_floats(M, g.KT);
   const int ndof = em_ndof(M, g.L);
   const int km = wpe ? wpe->taps * M : 0;
-  const int wtiles = wpe ? wpe_gram_tiles(km) : 0;
+  const int wcell = wpe ? wpe_gram_cell_elems(km, M) : 0;
   std::vector<unsigned char> h_pat;
   std::vector<uint32_t> h_masks;
   long long o_audio = 0, o_y = 0, o_g = 0, o_x = 0, o_wave = 0, o_tab = 0, o_coef = 0, o_cell = 0, o_fk = 0, o_f = 0,
@@ -403,7 +403,7 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
   }
   if (need.wpe) {
     g.w = m.get<float>(o_w);
-    g.gram = m.get<float2>((size_t)o_wcell * wtiles * 64);
+    g.gram = m.get<float2>((size_t)o_wcell * wcell);
     g.gconj = m.get<float2>(o_gw);
   }
   if (m.last != cudaSuccess) {

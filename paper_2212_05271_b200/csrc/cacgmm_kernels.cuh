@@ -111,6 +111,17 @@ struct PartLayout {
   static constexpr int CELL = L * STRIDE;
 };
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
@@ -132,6 +143,11 @@ __device__ __forceinline__ void cp_async_wait() {
 /// B^-1 coefficients live in shared memory ([lane g][class][NDOFP], NDOFP = NDOF rounded up to 4 so a
 /// lane fetches them as float4); that keeps the register tile to the accumulators and lets two CTAs
 /// share an SM when the accumulators are small enough.
+/// Sweep flavours: kSweepEM accumulates the M-step Grams; kSweepEMGamma does the same and may also store
+/// the posteriors (last sweep of the stage entry point); kSweepFinal accumulates the MVDR statistics and
+/// may store the posteriors (last sweep of enhance_batch).
+enum SweepMode { kSweepEM = 0, kSweepEMGamma = 1, kSweepFinal = 2 };
+
 template <int M, int L, int KT, bool FINAL>
 struct EmPassCfg {
   static constexpr int NDOF = EmLayout<M, L>::NDOF;
@@ -143,8 +159,10 @@ struct EmPassCfg {
   static constexpr int FS = LaneMap<M, L>::STRIDE;  // frame stride in the pipeline buffers
 };
 
-template <int M, int L, int KT, bool FINAL>
-__global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) em_pass_kernel(EmPassArgs a) {
+template <int M, int L, int KT, int MODE>
+__global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweepFinal>::MINB)
+    em_pass_kernel(EmPassArgs a) {
+  constexpr bool FINAL = MODE == kSweepFinal;
   using Lay = EmLayout<M, L>;
   using Cfg = EmPassCfg<M, L, KT, FINAL>;
   constexpr int NA = FINAL ? 2 : KT;
@@ -208,7 +226,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
   double ll = 0.0;
   FramePlan<M, L> plan;
   plan.init(g);
-  float* gout = a.gamma != nullptr && sd.g_off >= 0
+  float* gout = MODE != kSweepEM && a.gamma != nullptr && sd.g_off >= 0
                     ? a.gamma + sd.g_off + ((long long)f * sd.T + t0) * sd.K
                     : nullptr;
   const int target = sd.target;
@@ -244,8 +262,8 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
       plan.dofs(sl + fbc * FS, pv);
       float inv2 = 1.f;
       if (normalize) {
-        const float nr = __fsqrt_rn(plan.norm2(pv)) + 1e-10f;  // wpe.hpp:135
-        const float inv = __frcp_rn(nr);
+        const float nr = sqrt_approx(plan.norm2(pv)) + 1e-10f;  // wpe.hpp:135
+        const float inv = rcp_approx(nr);
         inv2 = inv * inv;
       }
       float q[KT];
@@ -281,15 +299,17 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
         u[k] = __expf(u[k] - mx);
         se += u[k];
       }
-      const float rinv = valid ? __frcp_rn(se) : 0.f;
+      const float rinv = valid ? rcp_approx(se) : 0.f;
       if (valid && g == 0) ll += (double)(mx + __logf(se));
       float gam[KT];
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
         gam[k] = u[k] * rinv;  // exactly 0 for inactive classes
         mass[k] += gam[k];
-        if (gout != nullptr && valid && (k % L) == g && k < sd.K)
-          gout[(long long)(tile * TILE + fb) * sd.K + k] = gam[k];
+        if (MODE != kSweepEM) {
+          if (gout != nullptr && valid && (k % L) == g && k < sd.K)
+            gout[(long long)(tile * TILE + fb) * sd.K + k] = gam[k];
+        }
       }
       if (FINAL) {
         float wt = 0.f, wb = 0.f;
@@ -306,7 +326,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, FINAL>::MINB) 
       } else {
 #pragma unroll
         for (int k = 0; k < NA; ++k) {
-          const float w = gam[k] * inv2 * __frcp_rn(q[k]);  // gamma / q on the unit-norm frame
+          const float w = gam[k] * inv2 * rcp_approx(q[k]);  // gamma / q on the unit-norm frame
 #pragma unroll
           for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w, pv[j], acc[k][j]);
         }

@@ -49,7 +49,8 @@ struct WpeArgs {
   double regularization;
   int M, taps, delay, psd_context;
 };
-int wpe_gram_tiles(int km);
+/// cfloat elements of one (segment, bin, chunk) Gram cell
+int wpe_gram_cell_elems(int km, int M);
 /// one kernel of a WPE iteration; step: 0 power, 1 gram, 2 solve, 3 apply
 cudaError_t launch_wpe_step(int step, const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
                             cudaStream_t st);

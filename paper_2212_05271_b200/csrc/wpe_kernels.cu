@@ -29,25 +29,44 @@ constexpr int kGramWarps = 8;
 constexpr int kGramThreads = kGramWarps * 32;
 constexpr int kGramTileFrames = 512;  // frames staged per shared-memory tile
 
+// Output tiling of the Gram: R's lower triangle in row blocks of 8 window elements x column blocks of
+// kTC, followed by the cross term P (km x M) in the same row blocks x ceil(M/kTC) column blocks.
+constexpr int kTC = 4;                 // tile columns (8 x 4 complex accumulators = 64 registers per lane)
+constexpr int kTileElems = 8 * kTC;
+constexpr int kCPR = 8 / kTC;          // column blocks per row block on the diagonal
+
 __host__ __device__ inline int gram_row_blocks(int km) { return (km + 7) / 8; }
-__host__ __device__ inline int gram_num_tiles(int km) {
+__host__ __device__ inline int gram_tri_tiles(int nb) { return kCPR * nb * (nb + 1) / 2; }
+__host__ __device__ inline int gram_p_cols(int M) { return (M + kTC - 1) / kTC; }
+__host__ __device__ inline int gram_num_tiles(int km, int M) {
   const int nb = gram_row_blocks(km);
-  return nb * (nb + 1) / 2 + nb;
+  return gram_tri_tiles(nb) + nb * gram_p_cols(M);
+}
+/// tile holding R[i][j], j <= i
+__host__ __device__ inline int gram_r_tile(int i, int j) {
+  const int bi = i >> 3;
+  return kCPR * bi * (bi + 1) / 2 + j / kTC;
+}
+/// tile holding P[i][c]
+__host__ __device__ inline int gram_p_tile(int i, int c, int nb, int M) {
+  return gram_tri_tiles(nb) + (i >> 3) * gram_p_cols(M) + c / kTC;
 }
 
-/// tile index -> (row block, column block); column block == nb marks the
-/// cross-term tile against the current frame.
-__device__ __forceinline__ void gram_tile_coords(int tile, int nb, int& bi, int& bj) {
-  const int ntri = nb * (nb + 1) / 2;
+/// tile index -> (row block, column block, is-cross-term)
+__device__ __forceinline__ void gram_tile_coords(int tile, int nb, int M, int& bi, int& bj, bool& cross) {
+  const int ntri = gram_tri_tiles(nb);
   if (tile >= ntri) {
-    bi = tile - ntri;
-    bj = nb;
+    const int pc = gram_p_cols(M);
+    bi = (tile - ntri) / pc;
+    bj = (tile - ntri) % pc;
+    cross = true;
     return;
   }
   int r = 0;
-  while ((r + 1) * (r + 2) / 2 <= tile) ++r;
+  while (kCPR * (r + 1) * (r + 2) / 2 <= tile) ++r;
   bi = r;
-  bj = tile - r * (r + 1) / 2;
+  bj = tile - kCPR * r * (r + 1) / 2;
+  cross = false;
 }
 
 __device__ __forceinline__ void cp_async_bytes8(void* smem_dst, const void* gsrc) {
@@ -87,76 +106,72 @@ __global__ void __launch_bounds__(256) wpe_power_kernel(WpeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Weighted Gram. grid (tile groups * wchunks, F, segments), block 256.
-// Warp w of group g owns output tile g*8+w for the CTA's whole frame range;
-// lane l accumulates frames l, l+32, ... and the 32 lanes are summed at the end.
-// Shared slab: [channel][frame] (pitch odd) so a warp's loads are contiguous.
+// Weighted Gram. grid (tile groups * wchunks, F, segments), block 256, two CTAs per SM.
+// Warp w of group g owns output tile g*8+w (8 x kTC complex accumulators per lane) for the CTA's
+// whole frame range; lane l accumulates frames l, l+32, ... and the 32 lanes are summed at the end.
 // ---------------------------------------------------------------------------
 template <int M>
-__global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
+__global__ void __launch_bounds__(kGramThreads, 2) wpe_gram_kernel(WpeArgs a) {
   extern __shared__ float4 smem_f4[];
   const SegDev sd = a.segs[blockIdx.z];
   if (!sd.wpe_active) return;
   const int f = blockIdx.y;
-  const int km = a.taps * M, nb = gram_row_blocks(km), ntiles = gram_num_tiles(km);
+  const int km = a.taps * M, nb = gram_row_blocks(km), ntiles = gram_num_tiles(km, M);
   const int ngroups = (ntiles + kGramWarps - 1) / kGramWarps;
   const int group = blockIdx.x % ngroups, chunk = blockIdx.x / ngroups;
   if (chunk >= sd.wchunks) return;
   const int H = a.delay + a.taps - 1;
-  const int SF = kGramTileFrames + H;      // slab frames per tile (history halo first)
-  const int pitch = SF | 1;
-  const int buf_floats = 2 * M * pitch + kGramTileFrames;       // one pipeline stage: slab + weights
+  // Frame-major slab with an odd frame stride: the window of a frame is a contiguous slice, so a lane
+  // addresses its 8 rows / kTC columns as base + immediate, and lanes (= consecutive frames) hit
+  // distinct bank pairs.
+  constexpr int S = M | 1;
+  const int slab_frames = kGramTileFrames + H + 8;  // + 8: padded rows / columns of the last blocks look ahead
+  const int buf_floats = 2 * S * slab_frames + kGramTileFrames;  // one pipeline stage: slab + weights
   float* stage0 = reinterpret_cast<float*>(smem_f4);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = group * kGramWarps + warp;
   const bool live = tile < ntiles;
   int bi = 0, bj = 0;
-  if (live) gram_tile_coords(tile, nb, bi, bj);
-  int rowoff[8], coloff[8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    // rows / columns past km (padding of the last block) alias the last valid
-    // element; their outputs are never read
-    const int e = min(8 * bi + r, km - 1);
-    rowoff[r] = (e % M) * pitch + e / M;
-    if (bj == nb) {
-      coloff[r] = (r < M ? r : 0) * pitch + H;
-    } else {
-      const int e2 = min(8 * bj + r, km - 1);
-      coloff[r] = (e2 % M) * pitch + e2 / M;
-    }
-  }
-  float accr[8][8], acci[8][8];
+  bool cross = false;
+  if (live) gram_tile_coords(tile, nb, M, bi, bj, cross);
+  const int row0 = 8 * bi;                                  // window element of the first row
+  const int col0 = cross ? H * S + kTC * bj : kTC * bj;     // slab offset of the first column
+  float accr[8][kTC], acci[8][kTC];
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) accr[r][c] = acci[r][c] = 0.f;
+    for (int c = 0; c < kTC; ++c) accr[r][c] = acci[r][c] = 0.f;
 
   const int t_begin = chunk * sd.WTC, t_end = min(sd.T, t_begin + sd.WTC);
   const float2* yf = a.yobs + sd.y_off + (long long)f * sd.T * M;
   const float* wf = a.w + sd.w_off + (long long)f * sd.T;
   const int ntl = (t_end - t_begin + kGramTileFrames - 1) / kGramTileFrames;
 
-  // stage frames [tb-H, tb+nfr) channel-major (a transposing cp.async per element);
-  // frames < 0 are zero (wpe.hpp:74-75)
+  // stage frames [tb-H, tb+nfr+8); frames < 0 or >= T are zero (wpe.hpp:74-75)
   auto issue = [&](int tl, int buf) {
     const int tb = t_begin + tl * kGramTileFrames;
     const int nfr = min(kGramTileFrames, t_end - tb);
     float2* slab = reinterpret_cast<float2*>(stage0 + buf * buf_floats);
-    float* wsm = stage0 + buf * buf_floats + 2 * M * pitch;
-    for (int i = tid; i < (nfr + H) * M; i += kGramThreads) {
+    float* wsm = stage0 + buf * buf_floats + 2 * S * slab_frames;
+    for (int i = tid; i < (nfr + H + 8) * M; i += kGramThreads) {
       const int fr = i / M, c = i - fr * M;
       const int t = tb - H + fr;
-      if (t >= 0)
-        cp_async_bytes8(slab + c * pitch + fr, yf + (long long)t * M + c);
+      if (t >= 0 && t < sd.T)
+        cp_async_bytes8(slab + fr * S + c, yf + (long long)t * M + c);
       else
-        slab[c * pitch + fr] = make_float2(0.f, 0.f);
+        slab[fr * S + c] = make_float2(0.f, 0.f);
     }
     for (int i = tid; i < nfr; i += kGramThreads) cp_async_bytes4(wsm + i, wf + tb + i);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
+  if (S != M) {  // the pad column is read by the cross-term tiles' unused columns: keep it finite
+    for (int i = tid; i < 2 * slab_frames; i += kGramThreads) {
+      float2* slab = reinterpret_cast<float2*>(stage0 + (i / slab_frames) * buf_floats);
+      slab[(i % slab_frames) * S + (S - 1)] = make_float2(0.f, 0.f);
+    }
+  }
   issue(0, 0);
   for (int tl = 0; tl < ntl; ++tl) {
     const int buf = tl & 1;
@@ -169,22 +184,24 @@ __global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
     __syncthreads();
     const int nfr = min(kGramTileFrames, t_end - (t_begin + tl * kGramTileFrames));
     const float2* slab = reinterpret_cast<const float2*>(stage0 + buf * buf_floats);
-    const float* wsm = stage0 + buf * buf_floats + 2 * M * pitch;
+    const float* wsm = stage0 + buf * buf_floats + 2 * S * slab_frames;
     if (live) {
       for (int fi = lane; fi < nfr; fi += 32) {
         const float w = wsm[fi];
-        float2 ar[8], bc[8];
+        const float2* rp = slab + fi * S + row0;
+        const float2* cp = slab + fi * S + col0;
+        float2 ar[8], bc[kTC];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) ar[r] = slab[rowoff[r] + fi];
+        for (int r = 0; r < 8; ++r) ar[r] = rp[r];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float2 v = slab[coloff[c] + fi];
+        for (int c = 0; c < kTC; ++c) {
+          const float2 v = cp[c];
           bc[c] = make_float2(v.x * w, v.y * w);
         }
 #pragma unroll
         for (int r = 0; r < 8; ++r)
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < kTC; ++c) {
             // a * conj(b)
             accr[r][c] = fmaf(ar[r].x, bc[c].x, accr[r][c]);
             accr[r][c] = fmaf(ar[r].y, bc[c].y, accr[r][c]);
@@ -201,17 +218,17 @@ __global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < kTC; ++c) {
         accr[r][c] += __shfl_xor_sync(0xffffffffu, accr[r][c], o);
         acci[r][c] += __shfl_xor_sync(0xffffffffu, acci[r][c], o);
       }
-  float2* out = a.gram + ((sd.wcell_off + (long long)f * sd.wchunks + chunk) * ntiles + tile) * 64;
-  // lane l writes entries l and l+32 (static register indices: select by predicate)
+  float2* out = a.gram + ((sd.wcell_off + (long long)f * sd.wchunks + chunk) * ntiles + tile) * kTileElems;
+  // lane l writes entry l (static register indices: select by predicate)
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int idx = r * 8 + c;
+    for (int c = 0; c < kTC; ++c) {
+      const int idx = r * kTC + c;
       if ((idx & 31) == lane) out[idx] = make_float2(accr[r][c], acci[r][c]);
     }
 }
@@ -226,24 +243,21 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
   const SegDev sd = a.segs[blockIdx.y];
   if (!sd.wpe_active) return;
   const int f = blockIdx.x;
-  const int M = a.M, km = a.taps * M, nb = gram_row_blocks(km), ntiles = gram_num_tiles(km);
-  const int ntri = nb * (nb + 1) / 2;
+  const int M = a.M, km = a.taps * M, nb = gram_row_blocks(km), ntiles = gram_num_tiles(km, M);
   const int ld = km + 1;
   cdbl* A = reinterpret_cast<cdbl*>(smem_f4);  // km x ld
   cdbl* B = A + (size_t)km * ld;               // km x M
   __shared__ double s_tr;
   __shared__ int s_fail;
   const int tid = threadIdx.x, nth = blockDim.x;
-  const float2* tiles = a.gram + (sd.wcell_off + (long long)f * sd.wchunks) * ntiles * 64;
-  const long long chunk_stride = (long long)ntiles * 64;
+  const float2* tiles = a.gram + (sd.wcell_off + (long long)f * sd.wchunks) * ntiles * kTileElems;
+  const long long chunk_stride = (long long)ntiles * kTileElems;
 
   // lower triangle of R (upper mirrored by hermitize) and P, summed over chunks in double
   for (int idx = tid; idx < km * km; idx += nth) {
     const int i = idx / km, j = idx - i * km;
     if (j > i) continue;
-    const int bi = i >> 3, bj = j >> 3;
-    const int tile = bi * (bi + 1) / 2 + bj;
-    const float2* p = tiles + (long long)tile * 64 + (i & 7) * 8 + (j & 7);
+    const float2* p = tiles + (long long)gram_r_tile(i, j) * kTileElems + (i & 7) * kTC + j % kTC;
     double re = 0.0, im = 0.0;
     for (int c = 0; c < sd.wchunks; ++c) {
       const float2 v = p[c * chunk_stride];
@@ -257,8 +271,7 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
   }
   for (int idx = tid; idx < km * M; idx += nth) {
     const int i = idx / M, c = idx - i * M;
-    const int tile = ntri + (i >> 3);
-    const float2* p = tiles + (long long)tile * 64 + (i & 7) * 8 + c;
+    const float2* p = tiles + (long long)gram_p_tile(i, c, nb, M) * kTileElems + (i & 7) * kTC + c % kTC;
     double re = 0.0, im = 0.0;
     for (int ch = 0; ch < sd.wchunks; ++ch) {
       const float2 v = p[ch * chunk_stride];
@@ -400,7 +413,7 @@ __global__ void __launch_bounds__(256) wpe_apply_kernel(WpeArgs a) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-int wpe_gram_tiles(int km) { return gram_num_tiles(km); }
+int wpe_gram_cell_elems(int km, int M) { return gram_num_tiles(km, M) * kTileElems; }
 
 template <int M>
 static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
@@ -410,8 +423,8 @@ static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F
     dim3 grid((max_frames + 255) / 256, F, nseg);
     wpe_power_kernel<<<grid, 256, 0, st>>>(a);
   } else if (step == 1) {
-    const int ngroups = (gram_num_tiles(km) + kGramWarps - 1) / kGramWarps;
-    const size_t smem = 2 * (sizeof(float2) * (size_t)M * ((kGramTileFrames + H) | 1) + sizeof(float) * kGramTileFrames);
+    const int ngroups = (gram_num_tiles(km, M) + kGramWarps - 1) / kGramWarps;
+    const size_t smem = 2 * (sizeof(float2) * (size_t)(M | 1) * (kGramTileFrames + H + 8) + sizeof(float) * kGramTileFrames);
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(wpe_gram_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -287,3 +287,24 @@ def test_numerics_rank_deficient_background_uses_eigen_floor(gss, oracle):
     wh, wz = oracle.mvdr(tgt, bg, 0)
     assert np.isfinite(flt.h).all() and flt.zeroed_bins == wz
     assert rel_fro(flt.h, wh) < 1e-3
+    # indefinite background: Cholesky fails, the device runs the Jacobi eigenvalue-floor fallback
+    # (numerics.hpp:58-73, 90-93) and must agree with the oracle's fallback
+    rng = np.random.RandomState(3)
+    for m in (2, 4, 7, 8):
+        q, _ = np.linalg.qr(rng.randn(m, m) + 1j * rng.randn(m, m))
+        lam = np.linspace(-1.0, 3.0, m)
+        bg = ((q * lam) @ q.conj().T)[None]
+        bg = 0.5 * (bg + bg.conj().transpose(0, 2, 1))
+        r = rng.randn(m, m) + 1j * rng.randn(m, m)
+        tgt = (r @ r.conj().T)[None]
+        flt = gss.beamform.mvdr(gss.beamform.BeamformerStats(tgt, bg, 1), 1 % m)
+        wh, wz = oracle.mvdr(tgt, bg, 1 % m)
+        assert flt.zeroed_bins == wz
+        assert rel_fro(flt.h, wh) < 1e-6, (m, rel_fro(flt.h, wh))
+    # no positive eigenvalue at all -> SingularMatrixError carrying the bin (test_numerics.cpp:140-148)
+    bad = np.zeros((40, 3, 3), np.complex128)
+    bad[:] = np.eye(3)
+    bad[37] = -np.eye(3)
+    with pytest.raises(gss.SingularMatrixError) as e:
+        gss.beamform.mvdr(gss.beamform.BeamformerStats(bad, bad, 1), 0)
+    assert e.value.frequency() == 37
