@@ -116,6 +116,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+__device__ __forceinline__ float lg2_approx(float x) {  // x >= 1e-10 here: no denormal inputs
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
   asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -290,17 +300,19 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
         q[k] = fmaxf(q[k] * inv2, kQuadFloor);               // cacgmm.hpp:170-171
-        u[k] = fmaf(-(float)M, __logf(q[k]), ckp[k]);         // inactive classes carry ck = -inf
+        // log2 domain: the table holds ck * log2(e); inactive classes carry ck = -inf
+        u[k] = fmaf(-(float)M, lg2_approx(q[k]), ckp[k]);
         mx = fmaxf(mx, u[k]);
       }
       float se = 0.f;
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
-        u[k] = __expf(u[k] - mx);
+        u[k] = ex2_approx(u[k] - mx);
         se += u[k];
       }
       const float rinv = valid ? rcp_approx(se) : 0.f;
-      if (valid && g == 0) ll += (double)(mx + __logf(se));
+      if (valid && g == 0) ll += (double)(mx + lg2_approx(se));  // log2 units, scaled once at the end
+      const float rinv2 = rinv * inv2;
       float gam[KT];
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
@@ -326,7 +338,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
       } else {
 #pragma unroll
         for (int k = 0; k < NA; ++k) {
-          const float w = gam[k] * inv2 * rcp_approx(q[k]);  // gamma / q on the unit-norm frame
+          const float w = u[k] * rinv2 * rcp_approx(q[k]);  // gamma / q on the unit-norm frame
 #pragma unroll
           for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w, pv[j], acc[k][j]);
         }
@@ -340,7 +352,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
   }
 
   // ---- reduce: frame slots within the warp, then warps through shared memory
-  if (g != 0) ll = 0.0;
+  ll = g != 0 ? 0.0 : ll * 0.69314718055994530942;  // back to natural-log units
 #pragma unroll
   for (int o = LM::S_LO; o < LM::S_HI; o <<= 1) {
 #pragma unroll
@@ -383,46 +395,87 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
 }
 
 // ---------------------------------------------------------------------------
-// M-step finalisation / state preparation. grid = (ceil(F/BPB), segments),
-// block = (KT, BPB). Thread (k, b) owns class k of bin f.
+// M-step finalisation / state preparation. grid = (F, segments), block = KT warps: warp k owns class k
+// of the bin, its M x M matrices live in shared memory and the lanes work on entries / column solves
+// in parallel (the single-thread form of the same algebra is latency bound: ~100 us per launch).
 // ---------------------------------------------------------------------------
-constexpr int kUpdateBinsPerBlock = 16;
+/// In-place lower Cholesky of the Hermitian M x M matrix f (row-major, shared memory) by one warp.
+/// Fails (returns false) iff a pivot is <= 0, Eigen LLT's criterion (numerics.hpp:88,105).
+template <int M>
+__device__ __forceinline__ bool warp_cholesky(cdbl* f, int lane) {
+  for (int k = 0; k < M; ++k) {
+    const double d = f[k * M + k].re;
+    if (!(d > 0.0)) return false;  // warp-uniform
+    const double sq = sqrt(d), inv = 1.0 / sq;
+    __syncwarp();
+    if (lane == 0) f[k * M + k] = cd_make(sq, 0.0);
+    if (lane > k && lane < M) f[lane * M + k] = cd_scale(f[lane * M + k], inv);
+    __syncwarp();
+    const int r = M - 1 - k;
+    if (lane < r * (r + 1) / 2) {
+      int ii = 0;
+      while ((ii + 1) * (ii + 2) / 2 <= lane) ++ii;
+      const int i = k + 1 + ii, j = k + 1 + (lane - ii * (ii + 1) / 2);
+      f[i * M + j] = cd_sub(f[i * M + j], cd_mulc(f[i * M + k], f[j * M + k]));
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+/// inv <- (L L^H)^-1, lane c solves column c (forward then backward substitution).
+template <int M>
+__device__ __forceinline__ void warp_cholesky_inverse(const cdbl* l, cdbl* inv, int lane) {
+  if (lane < M) {
+    const int c = lane;
+    for (int i = 0; i < M; ++i) {
+      cdbl s = cd_make(i == c ? 1.0 : 0.0, 0.0);
+      for (int j = 0; j < i; ++j) s = cd_sub(s, cd_mul(l[i * M + j], inv[j * M + c]));
+      inv[i * M + c] = cd_scale(s, 1.0 / l[i * M + i].re);
+    }
+    for (int i = M - 1; i >= 0; --i) {
+      cdbl s = inv[i * M + c];
+      for (int j = i + 1; j < M; ++j) s = cd_sub(s, cd_cmul(l[j * M + i], inv[j * M + c]));
+      inv[i * M + c] = cd_scale(s, 1.0 / l[i * M + i].re);
+    }
+  }
+  __syncwarp();
+}
 
 template <int M, int L, int KT>
-__global__ void em_update_kernel(EmUpdateArgs a) {
+__global__ void __launch_bounds__(KT * 32) em_update_kernel(EmUpdateArgs a) {
   using Lay = EmLayout<M, L>;
   using PL = PartLayout<M, L, KT, KT>;
   constexpr int NDOF = Lay::NDOF;
-  __shared__ double s_pi[kUpdateBinsPerBlock][KT];
-  __shared__ double s_ld[kUpdateBinsPerBlock][KT];
+  constexpr int MM = M * M;
+  __shared__ cdbl s_b[KT][MM], s_f[KT][MM], s_inv[KT][MM];
+  __shared__ double s_pi[KT], s_ld[KT];
 
-  const int k = threadIdx.x, b = threadIdx.y;
-  const int f = blockIdx.x * kUpdateBinsPerBlock + b;
-  const int seg = blockIdx.y;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.x, seg = blockIdx.y;
   const SegDev sd = a.segs[seg];
-  const bool in_bin = f < a.F;
-  const bool live = in_bin && k < sd.K;
-  const long long fk = sd.fk_off + (long long)(in_bin ? f : 0) * KT + k;
-  const long long cell0 = sd.cell_off + (long long)(in_bin ? f : 0) * sd.nchunks;
+  const bool live = k < sd.K;
+  const long long fk = sd.fk_off + (long long)f * KT + k;
+  const long long cell0 = sd.cell_off + (long long)f * sd.nchunks;
 
-  if (in_bin && k == 0 && (a.mode == kEmMstep || a.mode == kEmFinal)) {
+  if (threadIdx.x == 0 && (a.mode == kEmMstep || a.mode == kEmFinal)) {
     double ll = 0.0;
     for (int c = 0; c < sd.nchunks; ++c) ll += a.cell_ll[cell0 + c];
     a.bin_ll[sd.f_off + f] = ll;
   }
+  if (a.mode == kEmFinal) return;
 
   double my_pi = 0.0, my_ld = 0.0;
-  if (live && a.mode != kEmFinal) {
-    cdbl gram[M * M], inv[M * M], work[M * M], fact[M * M];
-    double wv[M];
-    bool have_b = false;      // gram holds the (new) shape matrix
+  cdbl* B = s_b[k];
+  if (live) {
+    bool have_b = false;      // B holds the (new) shape matrix
     bool need_invert = false;
     if (a.mode == kEmInit) {
-      for (int i = 0; i < M * M; ++i) gram[i] = cd_make((i / M == i % M) ? 1.0 : 0.0, 0.0);
+      for (int e = lane; e < MM; e += 32) B[e] = cd_make((e / M == e % M) ? 1.0 : 0.0, 0.0);
       my_pi = 1.0 / (double)sd.K;
       have_b = need_invert = true;
     } else if (a.mode == kEmFromState) {
-      for (int i = 0; i < M * M; ++i) gram[i] = a.bstate[fk * (M * M) + i];
+      for (int e = lane; e < MM; e += 32) B[e] = a.bstate[fk * MM + e];
       my_pi = a.pi[fk];
       need_invert = true;
     } else {
@@ -433,89 +486,126 @@ __global__ void em_update_kernel(EmUpdateArgs a) {
         my_pi = kWeightFloor;
         my_ld = a.logdet[fk];
       } else {
-        for (int i = 0; i < M * M; ++i) gram[i] = cd_make(0.0, 0.0);
-        for (int g = 0; g < L; ++g)
-          for (int j = 0; j < NDOF; ++j) {
-            const DofInfo di = dof_info(M, L, g, j);
-            if (di.kind == kIdle) continue;
-            double v = 0.0;
-            for (int c = 0; c < sd.nchunks; ++c)
-              v += (double)a.part[(cell0 + c) * a.cell_stride + g * PL::STRIDE + k * NDOF + j];
-            dof_scatter(gram, M, di, v);
-          }
+        for (int e = lane; e < MM; e += 32) B[e] = cd_make(0.0, 0.0);
+        __syncwarp();
+        // chunk partials -> Gram, summed in double in chunk order; both triangles are written from
+        // the same sums, so hermitize (cacgmm.hpp:330) is the identity on this matrix
+        for (int d = lane; d < L * NDOF; d += 32) {
+          const int g = d / NDOF, j = d - g * NDOF;
+          const DofInfo di = dof_info(M, L, g, j);
+          if (di.kind == kIdle) continue;
+          double v = 0.0;
+          for (int c = 0; c < sd.nchunks; ++c)
+            v += (double)a.part[(cell0 + c) * a.cell_stride + g * PL::STRIDE + k * NDOF + j];
+          dof_scatter(B, M, di, v);
+        }
+        __syncwarp();
         const double s = (double)M / mass;  // cacgmm.hpp:327-329
+        for (int e = lane; e < MM; e += 32) B[e] = cd_scale(B[e], s);
+        __syncwarp();
         double tr = 0.0;
-        for (int i = 0; i < M * M; ++i) gram[i] = cd_scale(gram[i], s);
-        hermitize_inplace(gram, M, M);
-        for (int i = 0; i < M; ++i) tr += gram[i * M + i].re;
+        for (int i = 0; i < M; ++i) tr += B[i * M + i].re;
+        __syncwarp();
         if (tr > 0.0) {
           const double gsc = (double)M / tr;
-          for (int i = 0; i < M * M; ++i) gram[i] = cd_scale(gram[i], gsc);
+          for (int e = lane; e < MM; e += 32) B[e] = cd_scale(B[e], gsc);
         }
-        regularize_inplace(gram, M, M, kRegEps);
+        __syncwarp();
+        double tr2 = 0.0;  // regularize (numerics.hpp:41-49)
+        for (int i = 0; i < M; ++i) tr2 += B[i * M + i].re;
+        double scale = tr2 / (double)M;
+        if (!(scale > 0.0)) scale = 1.0;
+        __syncwarp();
+        if (lane < M) B[lane * M + lane].re += kRegEps * scale;
         my_pi = fmax(kWeightFloor, mass / (double)sd.T);
         have_b = need_invert = true;
       }
     }
+    __syncwarp();
     if (have_b)
-      for (int i = 0; i < M * M; ++i) a.bstate[fk * (M * M) + i] = gram[i];
+      for (int e = lane; e < MM; e += 32) a.bstate[fk * MM + e] = B[e];
     if (need_invert) {
-      // invert_shapes: plain attempt, then once more on regularize(B) (cacgmm.hpp:134-140)
-      for (int i = 0; i < M * M; ++i) fact[i] = gram[i];
-      int st = hermitian_inverse_logdet<M>(fact, M, inv, &my_ld, work, wv);
-      if (st != kLinOk) {
-        for (int i = 0; i < M * M; ++i) fact[i] = gram[i];
-        regularize_inplace(fact, M, M, kRegEps);
-        st = hermitian_inverse_logdet<M>(fact, M, inv, &my_ld, work, wv);
-      }
-      if (st != kLinOk) {
-        atomicMin(&a.status[seg], make_status(5 /*SingularMatrixError*/, f));
-        my_ld = 0.0;
-        for (int i = 0; i < M * M; ++i) inv[i] = cd_make((i / M == i % M) ? 1.0 : 0.0, 0.0);
+      cdbl* F = s_f[k];
+      cdbl* inv = s_inv[k];
+      for (int e = lane; e < MM; e += 32) F[e] = B[e];
+      __syncwarp();
+      if (warp_cholesky<M>(F, lane)) {
+        double ld = 0.0;
+        for (int i = 0; i < M; ++i) ld += log(F[i * M + i].re);
+        my_ld = 2.0 * ld;
+        warp_cholesky_inverse<M>(F, inv, lane);
+      } else {
+        // rare path, one lane: eigenvalue-floor fallback, then the retry on regularize(B)
+        // (numerics.hpp:103-122, cacgmm.hpp:134-140)
+        __syncwarp();
+        if (lane == 0) {
+          cdbl fact[MM], work[MM], linv[MM];
+          double wv[M];
+          double ld = 0.0;
+          for (int i = 0; i < MM; ++i) fact[i] = B[i];
+          int st = hermitian_inverse_logdet<M>(fact, M, linv, &ld, work, wv);
+          if (st != kLinOk) {
+            for (int i = 0; i < MM; ++i) fact[i] = B[i];
+            regularize_inplace(fact, M, M, kRegEps);
+            st = hermitian_inverse_logdet<M>(fact, M, linv, &ld, work, wv);
+          }
+          if (st != kLinOk) {
+            atomicMin(&a.status[seg], make_status(5 /*SingularMatrixError*/, f));
+            ld = 0.0;
+            for (int i = 0; i < MM; ++i) linv[i] = cd_make((i / M == i % M) ? 1.0 : 0.0, 0.0);
+          }
+          for (int i = 0; i < MM; ++i) inv[i] = linv[i];
+          F[0].re = ld;
+        }
+        __syncwarp();
+        my_ld = F[0].re;
       }
       // B^-1 is rounded to cfloat before use (cacgmm.hpp:144-149)
-      for (int g = 0; g < L; ++g) {
-        float* cp = a.coef + sd.coef_off + ((long long)f * L + g) * (KT * NDOF) + k * NDOF;
-        for (int j = 0; j < NDOF; ++j) cp[j] = dof_coef(inv, M, dof_info(M, L, g, j));
+      for (int d = lane; d < L * NDOF; d += 32) {
+        const int g = d / NDOF, j = d - g * NDOF;
+        a.coef[sd.coef_off + ((long long)f * L + g) * (KT * NDOF) + k * NDOF + j] =
+            dof_coef(inv, M, dof_info(M, L, g, j));
       }
-      a.logdet[fk] = my_ld;
+      if (lane == 0) a.logdet[fk] = my_ld;
     }
-    a.pi[fk] = my_pi;
-  } else if (in_bin && (a.mode == kEmInit || a.mode == kEmFromState)) {
+    if (lane == 0) a.pi[fk] = my_pi;
+  } else if (a.mode == kEmInit || a.mode == kEmFromState) {
     // padded class (K <= k < KT): zero coefficients; it is masked off by ck = -inf
-    for (int g = 0; g < L; ++g) {
-      float* cp = a.coef + sd.coef_off + ((long long)f * L + g) * (KT * NDOF) + k * NDOF;
-      for (int j = 0; j < NDOF; ++j) cp[j] = 0.f;
+    for (int d = lane; d < L * NDOF; d += 32) {
+      const int g = d / NDOF, j = d - g * NDOF;
+      a.coef[sd.coef_off + ((long long)f * L + g) * (KT * NDOF) + k * NDOF + j] = 0.f;
     }
   }
-  s_pi[b][k] = my_pi;
-  s_ld[b][k] = my_ld;
+  if (lane == 0) {
+    s_pi[k] = my_pi;
+    s_ld[k] = my_ld;
+  }
   __syncthreads();
-  if (!in_bin || a.mode == kEmFinal) return;
 
   // E-step constants per activity pattern (cacgmm.hpp:196-237):
   //   ck = lp + c0 - log|B_k|, lp = log max(1e-10, pi_k) - log z, z = sum of active pi
   const double c0 = -(double)M * log(2.0 * 3.14159265358979323846) + lgamma((double)M);
   float* tab = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
-  for (int p = 0; p < sd.npat; ++p) {
+  for (int idx = threadIdx.x; idx < sd.npat * KT; idx += KT * 32) {
+    const int p = idx / KT, kk = idx - p * KT;
     const uint32_t mask = a.masks[sd.mask_off + p];
     float v = -CUDART_INF_F;
-    if (k < sd.K) {
+    if (kk < sd.K) {
       double z = 0.0;
-      for (int kk = 0; kk < sd.K; ++kk)
-        if (mask & (1u << kk)) z += s_pi[b][kk];
+      for (int q = 0; q < sd.K; ++q)
+        if (mask & (1u << q)) z += s_pi[q];
       bool active;
       double lp;
       if (z <= 0.0) {  // no active class: noise class alone, or uniform (cacgmm.hpp:217-226)
-        active = sd.noise >= 0 ? k == sd.noise : true;
+        active = sd.noise >= 0 ? kk == sd.noise : true;
         lp = sd.noise >= 0 ? 0.0 : -log((double)sd.K);
       } else {
-        active = (mask >> k) & 1u;
-        lp = log(fmax(kWeightFloor, s_pi[b][k])) - log(z);
+        active = (mask >> kk) & 1u;
+        lp = log(fmax(kWeightFloor, s_pi[kk])) - log(z);
       }
-      if (active) v = (float)(lp + c0 - s_ld[b][k]);
+      if (active) v = (float)((lp + c0 - s_ld[kk]) * 1.4426950408889634074);  // log2 units for the sweep
     }
-    tab[p * KT + k] = v;
+    tab[idx] = v;
   }
 }
 

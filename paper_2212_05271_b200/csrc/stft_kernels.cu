@@ -16,8 +16,10 @@ namespace gssb {
 
 namespace {
 
-constexpr int kStftThreads = 256;
+constexpr int kStftThreads = 256;   // inverse transform
 constexpr int kStftWarps = kStftThreads / 32;
+constexpr int kAnaThreads = 512;    // forward transform: 16 warps keep more FP64 FFTs in flight per SM
+constexpr int kAnaWarps = kAnaThreads / 32;
 
 /// In-place radix-2 DIT over bit-reversed input; tw[k] = exp(-2 pi i k / n).
 /// INVERSE conjugates the twiddles (unscaled inverse).
@@ -68,7 +70,7 @@ __device__ __forceinline__ long long reflect_index(long long idx, long long N) {
 // channels, assembles the (f, frame, channel) tile in shared memory and writes
 // runs of TB*M contiguous cfloats per bin (the (F,T,M) layout of stft.hpp:52-80).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kStftThreads) stft_kernel(StftArgs a) {
+__global__ void __launch_bounds__(kAnaThreads) stft_kernel(StftArgs a) {
   // The forward transform runs in FP64 like the reference's (stft.hpp:158-170,
   // double FFT then a cast to cfloat): an FP32 FFT leaves an error proportional
   // to the frame's LOUDEST bin in every bin, which the EM iterations amplify in
@@ -77,11 +79,14 @@ __global__ void __launch_bounds__(kStftThreads) stft_kernel(StftArgs a) {
   double2* fftbuf = reinterpret_cast<double2*>(smem_f4);
   const int n = a.p.fft_size, log2n = a.p.log2n, F = a.p.F, M = a.M, TB = a.TB, NFW = a.fft_warps;
   float2* tile = reinterpret_cast<float2*>(fftbuf + NFW * n);
+  double2* s_tw = reinterpret_cast<double2*>(tile + (size_t)F * ((TB * M) | 1) + (((size_t)F * ((TB * M) | 1)) & 1));
   const int run = TB * M;
   const int pitch = run | 1;
   const SegDev sd = a.segs[blockIdx.y];
   const int t0 = blockIdx.x * TB;
   if (t0 >= sd.T) return;
+  for (int i = threadIdx.x; i < n / 2; i += kAnaThreads) s_tw[i] = a.tw_d[i];
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pad = n / 2;
   const long long N = sd.N;
@@ -103,7 +108,7 @@ __global__ void __launch_bounds__(kStftThreads) stft_kernel(StftArgs a) {
       buf[__brev((unsigned)i) >> (32 - log2n)] = make_double2(r1, r2);
     }
     __syncwarp();
-    warp_fft<false>(buf, a.tw_d, n, log2n, lane);
+    warp_fft<false>(buf, s_tw, n, log2n, lane);
     for (int f = lane; f <= n / 2; f += 32) {
       const double2 zf = buf[f], zn = buf[(n - f) & (n - 1)];
       if (v1) tile[f * pitch + s1] = make_float2((float)(0.5 * (zf.x + zn.x)), (float)(0.5 * (zf.y - zn.y)));
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(kStftThreads) stft_kernel(StftArgs a) {
   __syncthreads();
   const int nvalid = min(TB, sd.T - t0) * M;
   float2* out = a.y + sd.y_off + (long long)t0 * M;
-  for (int e = threadIdx.x; e < F * nvalid; e += kStftThreads) {
+  for (int e = threadIdx.x; e < F * nvalid; e += kAnaThreads) {
     const int f = e / nvalid, r = e - f * nvalid;
     out[(long long)f * sd.T * M + r] = tile[f * pitch + r];
   }
@@ -231,20 +236,21 @@ __global__ void __launch_bounds__(kStftThreads) istft_kernel(IstftArgs a) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-static int stft_frames_per_cta(int n) { return n <= 512 ? 4096 / n : (n >= 2048 ? 1 : 2048 / n); }
-static int stft_fft_warps(int n) { return std::max(1, std::min(kStftWarps, 8192 / n)); }
+static int stft_frames_per_cta(int n) { return n >= 2048 ? 1 : 2048 / n; }
+static int stft_fft_warps(int n) { return std::max(1, std::min(kAnaWarps, 8192 / n)); }
 
 cudaError_t launch_stft(const StftArgs& args_in, int nseg, int max_frames, cudaStream_t st) {
   StftArgs a = args_in;
   a.TB = stft_frames_per_cta(a.p.fft_size);
   a.fft_warps = stft_fft_warps(a.p.fft_size);
-  const size_t smem = sizeof(double2) * (size_t)a.fft_warps * a.p.fft_size +
-                      sizeof(float2) * (size_t)a.p.F * ((a.TB * a.M) | 1);
+  const size_t tile_elems = (size_t)a.p.F * ((a.TB * a.M) | 1);
+  const size_t smem = sizeof(double2) * ((size_t)a.fft_warps * a.p.fft_size + a.p.fft_size / 2) +
+                      sizeof(float2) * (tile_elems + (tile_elems & 1));
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(stft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((max_frames + a.TB - 1) / a.TB, nseg);
-  stft_kernel<<<grid, kStftThreads, smem, st>>>(a);
+  stft_kernel<<<grid, kAnaThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -25,7 +25,7 @@ namespace gssb {
 
 namespace {
 
-constexpr int kGramWarps = 8;
+constexpr int kGramWarps = 16;  // one CTA of 16 warps per SM: the slab is staged once for 16 tiles
 constexpr int kGramThreads = kGramWarps * 32;
 constexpr int kGramTileFrames = 512;  // frames staged per shared-memory tile
 
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) wpe_power_kernel(WpeArgs a) {
 // whole frame range; lane l accumulates frames l, l+32, ... and the 32 lanes are summed at the end.
 // ---------------------------------------------------------------------------
 template <int M>
-__global__ void __launch_bounds__(kGramThreads, 2) wpe_gram_kernel(WpeArgs a) {
+__global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
   extern __shared__ float4 smem_f4[];
   const SegDev sd = a.segs[blockIdx.z];
   if (!sd.wpe_active) return;
@@ -121,12 +121,15 @@ __global__ void __launch_bounds__(kGramThreads, 2) wpe_gram_kernel(WpeArgs a) {
   const int group = blockIdx.x % ngroups, chunk = blockIdx.x / ngroups;
   if (chunk >= sd.wchunks) return;
   const int H = a.delay + a.taps - 1;
-  // Frame-major slab with an odd frame stride: the window of a frame is a contiguous slice, so a lane
-  // addresses its 8 rows / kTC columns as base + immediate, and lanes (= consecutive frames) hit
-  // distinct bank pairs.
-  constexpr int S = M | 1;
+  // Slab layout. Odd M: frame-major [frame][M]; the window of a frame is then ONE contiguous slice, a lane
+  // addresses its 8 rows / kTC columns as base + immediate, and lanes (= consecutive frames, odd stride)
+  // hit distinct bank pairs. Even M: that stride would be an 8-byte-bank multiple, so the slab is kept
+  // channel-major [channel][frame] (odd pitch) and every row / column carries its own offset.
+  constexpr bool CONTIG = (M & 1) != 0;
   const int slab_frames = kGramTileFrames + H + 8;  // + 8: padded rows / columns of the last blocks look ahead
-  const int buf_floats = 2 * S * slab_frames + kGramTileFrames;  // one pipeline stage: slab + weights
+  const int pitch = slab_frames | 1;
+  const int slab_elems = CONTIG ? M * slab_frames : M * pitch;
+  const int buf_floats = 2 * slab_elems + kGramTileFrames;  // one pipeline stage: slab + weights
   float* stage0 = reinterpret_cast<float*>(smem_f4);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -135,8 +138,28 @@ __global__ void __launch_bounds__(kGramThreads, 2) wpe_gram_kernel(WpeArgs a) {
   int bi = 0, bj = 0;
   bool cross = false;
   if (live) gram_tile_coords(tile, nb, M, bi, bj, cross);
-  const int row0 = 8 * bi;                                  // window element of the first row
-  const int col0 = cross ? H * S + kTC * bj : kTC * bj;     // slab offset of the first column
+  int rowoff[8], coloff[kTC];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    if (CONTIG) {
+      rowoff[r] = 8 * bi + r;  // window element = slab offset from the frame's window start
+    } else {
+      const int e = min(8 * bi + r, km - 1);  // padded rows alias the last valid element
+      rowoff[r] = (e % M) * pitch + e / M;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kTC; ++c) {
+    const int e = kTC * bj + c;
+    if (CONTIG) {
+      coloff[c] = cross ? H * M + e : e;  // unused columns of the last block read finite look-ahead data
+    } else if (cross) {
+      coloff[c] = (e < M ? e : 0) * pitch + H;
+    } else {
+      const int e2 = min(e, km - 1);
+      coloff[c] = (e2 % M) * pitch + e2 / M;
+    }
+  }
   float accr[8][kTC], acci[8][kTC];
 #pragma unroll
   for (int r = 0; r < 8; ++r)
@@ -153,25 +176,20 @@ __global__ void __launch_bounds__(kGramThreads, 2) wpe_gram_kernel(WpeArgs a) {
     const int tb = t_begin + tl * kGramTileFrames;
     const int nfr = min(kGramTileFrames, t_end - tb);
     float2* slab = reinterpret_cast<float2*>(stage0 + buf * buf_floats);
-    float* wsm = stage0 + buf * buf_floats + 2 * S * slab_frames;
+    float* wsm = stage0 + buf * buf_floats + 2 * slab_elems;
     for (int i = tid; i < (nfr + H + 8) * M; i += kGramThreads) {
       const int fr = i / M, c = i - fr * M;
       const int t = tb - H + fr;
+      float2* dst = slab + (CONTIG ? i : c * pitch + fr);
       if (t >= 0 && t < sd.T)
-        cp_async_bytes8(slab + fr * S + c, yf + (long long)t * M + c);
+        cp_async_bytes8(dst, yf + (long long)t * M + c);
       else
-        slab[fr * S + c] = make_float2(0.f, 0.f);
+        *dst = make_float2(0.f, 0.f);
     }
     for (int i = tid; i < nfr; i += kGramThreads) cp_async_bytes4(wsm + i, wf + tb + i);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
-  if (S != M) {  // the pad column is read by the cross-term tiles' unused columns: keep it finite
-    for (int i = tid; i < 2 * slab_frames; i += kGramThreads) {
-      float2* slab = reinterpret_cast<float2*>(stage0 + (i / slab_frames) * buf_floats);
-      slab[(i % slab_frames) * S + (S - 1)] = make_float2(0.f, 0.f);
-    }
-  }
   issue(0, 0);
   for (int tl = 0; tl < ntl; ++tl) {
     const int buf = tl & 1;
@@ -184,18 +202,17 @@ __global__ void __launch_bounds__(kGramThreads, 2) wpe_gram_kernel(WpeArgs a) {
     __syncthreads();
     const int nfr = min(kGramTileFrames, t_end - (t_begin + tl * kGramTileFrames));
     const float2* slab = reinterpret_cast<const float2*>(stage0 + buf * buf_floats);
-    const float* wsm = stage0 + buf * buf_floats + 2 * S * slab_frames;
+    const float* wsm = stage0 + buf * buf_floats + 2 * slab_elems;
     if (live) {
       for (int fi = lane; fi < nfr; fi += 32) {
         const float w = wsm[fi];
-        const float2* rp = slab + fi * S + row0;
-        const float2* cp = slab + fi * S + col0;
+        const float2* base = slab + (CONTIG ? fi * M : fi);
         float2 ar[8], bc[kTC];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) ar[r] = rp[r];
+        for (int r = 0; r < 8; ++r) ar[r] = CONTIG ? base[rowoff[0] + r] : base[rowoff[r]];
 #pragma unroll
         for (int c = 0; c < kTC; ++c) {
-          const float2 v = cp[c];
+          const float2 v = CONTIG ? base[coloff[0] + c] : base[coloff[c]];
           bc[c] = make_float2(v.x * w, v.y * w);
         }
 #pragma unroll
@@ -424,7 +441,7 @@ static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F
     wpe_power_kernel<<<grid, 256, 0, st>>>(a);
   } else if (step == 1) {
     const int ngroups = (gram_num_tiles(km, M) + kGramWarps - 1) / kGramWarps;
-    const size_t smem = 2 * (sizeof(float2) * (size_t)(M | 1) * (kGramTileFrames + H + 8) + sizeof(float) * kGramTileFrames);
+    const size_t smem = 2 * (sizeof(float2) * (size_t)M * ((kGramTileFrames + H + 8) | 1) + sizeof(float) * kGramTileFrames);
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(wpe_gram_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
