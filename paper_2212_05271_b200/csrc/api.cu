@@ -64,6 +64,7 @@ struct gss_b200_ctx {
   std::vector<ProfRec> prof_recs;
   double kernel_ms[GSS_B200_NUM_KERNELS] = {0};
   long long kernel_launches[GSS_B200_NUM_KERNELS] = {0};
+  int wpe_gram_tc = 1;       // GSS_B200_WPE_GRAM=fp32 selects the FP32-FMA Gram kernel instead of tcgen05
   int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
   int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
 };
@@ -251,6 +252,8 @@ struct Group {
   float2* hconj = nullptr;
   float* w = nullptr;
   float2 *gram = nullptr, *gconj = nullptr;
+  float* gram_raw = nullptr;
+  int use_tc = 0;
   status_t* status = nullptr;
   int *ref = nullptr, *zeroed = nullptr;
   long long tot_audio = 0, tot_y = 0, tot_g = 0, tot_x = 0, tot_wave = 0, tot_pat = 0, tot_mask = 0;
@@ -403,7 +406,11 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
   }
   if (need.wpe) {
     g.w = m.get<float>(o_w);
-    g.gram = m.get<float2>((size_t)o_wcell * wcell);
+    g.use_tc = c->wpe_gram_tc && wpe_tc_supported(km, M) && g.max_wchunks == 1;
+    if (g.use_tc)
+      g.gram_raw = m.get<float>((size_t)o_f * wpe_tc_cell_floats(km, M));
+    else
+      g.gram = m.get<float2>((size_t)o_wcell * wcell);
     g.gconj = m.get<float2>(o_gw);
   }
   if (m.last != cudaSuccess) {
@@ -444,6 +451,9 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
   a.yout = g.Yd;
   a.w = g.w;
   a.gram = g.gram;
+  a.gram_raw = g.gram_raw;
+  a.use_tc = g.use_tc;
+  a.debug_rp = nullptr;
   a.gconj = g.gconj;
   a.segs = g.d_segs;
   a.status = g.status;
@@ -639,6 +649,7 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
     unsigned long long thr = ~0ull;  // keep freed blocks cached for the next batch
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
+  if (const char* s = std::getenv("GSS_B200_WPE_GRAM")) c->wpe_gram_tc = std::strcmp(s, "fp32") != 0;
   if (const char* s = std::getenv("GSS_B200_EM_CHUNK_FRAMES")) c->em_chunk_frames = std::atoi(s);
   if (const char* s = std::getenv("GSS_B200_WPE_CHUNK_FRAMES")) c->wpe_chunk_frames = std::atoi(s);
   *out = c;
@@ -1228,6 +1239,51 @@ gss_status gss_b200_wpe(gss_b200_ctx* c, const float* in, int32_t bins, int64_t 
   rc = device_status(c, sg.g);
   if (rc != GSS_OK) return rc;
   CU_TRY(c, cudaMemcpyAsync(out, sg.g.Yd, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  return GSS_OK;
+}
+
+// Test hook (not in the public header): weights from `in`, one Gram pass, hermitized R and P per bin as cdouble.
+gss_status gss_b200_debug_wpe_gram(gss_b200_ctx* c, const float* in, int32_t bins, int64_t T, int32_t M,
+                                   const gss_wpe_config* cfg, double* out_rp) {
+  gss_status rc = check_tensor(c, bins, T, M);
+  if (rc != GSS_OK) return rc;
+  CU_TRY(c, cudaSetDevice(c->device));
+  StageGroup sg(c);
+  SegSpec s;
+  s.T = (int)T;
+  Needs need;
+  need.y = need.yd = need.wpe = true;
+  rc = build_group(c, sg.g, M, 1, bins, {s}, need, cfg, 0);
+  if (rc != GSS_OK) return rc;
+  Group& g = sg.g;
+  const int km = cfg->taps * M;
+  const size_t per = (size_t)km * km + (size_t)km * M;
+  cdbl* d_rp = g.mem.get<cdbl>(per * bins);
+  if (!d_rp) return fail(c, GSS_CUDA_ERROR, "alloc");
+  CU_TRY(c, cudaMemcpyAsync(g.Y, in, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyHostToDevice, c->stream));
+  WpeArgs a;
+  a.yobs = g.Y;
+  a.ycur = g.Y;
+  a.yout = g.Yd;
+  a.w = g.w;
+  a.gram = g.gram;
+  a.gram_raw = g.gram_raw;
+  a.use_tc = g.use_tc;
+  a.debug_rp = d_rp;
+  a.gconj = g.gconj;
+  a.segs = g.d_segs;
+  a.status = g.status;
+  a.regularization = cfg->regularization;
+  a.M = M;
+  a.taps = cfg->taps;
+  a.delay = cfg->delay;
+  a.psd_context = cfg->psd_context;
+  for (int step = 0; step < 3; ++step) {
+    KClock k(c, kK_wpe_power + step);
+    CU_TRY(c, launch_wpe_step(step, a, 1, bins, (int)T, g.max_wchunks, c->stream));
+  }
+  CU_TRY(c, cudaMemcpyAsync(out_rp, d_rp, sizeof(cdbl) * per * bins, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   return GSS_OK;
 }

@@ -42,15 +42,23 @@ struct WpeArgs {
   const float2* ycur;   // current estimate (power source)
   float2* yout;         // next estimate
   float* w;             // (F,T) weights
-  float2* gram;         // tiles
+  float2* gram;         // tiles (FP32 path)
+  float* gram_raw;      // raw real accumulators (tensor-core path): (F, 128, NCT) per segment
   float2* gconj;        // (F, km, M)
   const SegDev* segs;
   status_t* status;
   double regularization;
   int M, taps, delay, psd_context;
+  cdbl* debug_rp;       // non-null: the solve kernel only dumps hermitized R (km x km) and P (km x M) per bin
+  int use_tc;           // 1: the Gram of this iteration came from wpe_gram_tc_kernel
 };
 /// cfloat elements of one (segment, bin, chunk) Gram cell
 int wpe_gram_cell_elems(int km, int M);
+/// tensor-core Gram (wpe_gram_tc.cu)
+int wpe_tc_supported(int km, int M);
+int wpe_tc_cell_floats(int km, int M);
+int wpe_tc_rows(int km, int M);
+cudaError_t launch_wpe_gram_tc(const WpeArgs& a, int nseg, int F, cudaStream_t st);
 /// one kernel of a WPE iteration; step: 0 power, 1 gram, 2 solve, 3 apply
 cudaError_t launch_wpe_step(int step, const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
                             cudaStream_t st);

@@ -270,6 +270,30 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
   const float2* tiles = a.gram + (sd.wcell_off + (long long)f * sd.wchunks) * ntiles * kTileElems;
   const long long chunk_stride = (long long)ntiles * kTileElems;
 
+  if (a.use_tc) {
+    // raw real accumulators of the tensor-core Gram (wpe_gram_tc.cu): D1 = S[0..128) S^T (NR columns),
+    // D2 = S[NR-128..NR) S[128..NR)^T (N2 columns); G(a,b) by symmetry
+    const int NR = wpe_tc_rows(km, M), N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
+    const float* raw = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT);
+    auto G = [&](int x, int y) -> double {
+      if (x < 128) return (double)raw[x * NCT + y];
+      if (y < 128) return (double)raw[y * NCT + x];
+      return (double)raw[(x - (NR - 128)) * NCT + NR + (y - 128)];
+    };
+    for (int idx = tid; idx < km * km; idx += nth) {
+      const int i = idx / km, j = idx - i * km;
+      if (j > i) continue;
+      const double re = G(i, j) + G(km + i, km + j);
+      const double im = i == j ? 0.0 : G(km + i, j) - G(i, km + j);
+      A[i * ld + j] = cd_make(re, im);
+      A[j * ld + i] = cd_make(re, -im);
+    }
+    for (int idx = tid; idx < km * M; idx += nth) {
+      const int i = idx / M, c = idx - i * M;
+      B[i * M + c] = cd_make(G(i, 2 * km + c) + G(km + i, 2 * km + M + c),
+                             G(km + i, 2 * km + c) - G(i, 2 * km + M + c));
+    }
+  } else {
   // lower triangle of R (upper mirrored by hermitize) and P, summed over chunks in double
   for (int idx = tid; idx < km * km; idx += nth) {
     const int i = idx / km, j = idx - i * km;
@@ -297,8 +321,15 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
     }
     B[i * M + c] = cd_make(re, im);
   }
+  }
   if (tid == 0) s_fail = 0;
   __syncthreads();
+  if (a.debug_rp != nullptr) {  // test hook: expose the assembled Gram
+    cdbl* o = a.debug_rp + (long long)f * (km * km + km * M);
+    for (int idx = tid; idx < km * km; idx += nth) o[idx] = A[(idx / km) * ld + idx % km];
+    for (int idx = tid; idx < km * M; idx += nth) o[km * km + idx] = B[idx];
+    return;
+  }
   if (tid == 0) {  // regularize (numerics.hpp:41-49)
     double tr = 0.0;
     for (int i = 0; i < km; ++i) tr += A[i * ld + i].re;
@@ -439,6 +470,8 @@ static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F
   if (step == 0) {
     dim3 grid((max_frames + 255) / 256, F, nseg);
     wpe_power_kernel<<<grid, 256, 0, st>>>(a);
+  } else if (step == 1 && a.use_tc) {
+    return launch_wpe_gram_tc(a, nseg, F, st);
   } else if (step == 1) {
     const int ngroups = (gram_num_tiles(km, M) + kGramWarps - 1) / kGramWarps;
     const size_t smem = 2 * (sizeof(float2) * (size_t)M * ((kGramTileFrames + H + 8) | 1) + sizeof(float) * kGramTileFrames);
