@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
   if (a.use_tc) {
     // raw real accumulators of the tensor-core Gram (wpe_gram_tc.cu): D1 = S[0..128) S^T (NR columns),
     // D2 = S[NR-128..NR) S[128..NR)^T (N2 columns); G(a,b) by symmetry
-    const int NR = wpe_tc_rows(km, M), N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
+    const int NR = ((2 * km + 2 * M + 15) / 16) * 16, N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
     const float* raw = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT);
     auto G = [&](int x, int y) -> double {
       if (x < 128) return (double)raw[x * NCT + y];
