@@ -16,6 +16,8 @@
 // the canonical no-swizzle K-major core-matrix layout (a warp store = one 8x16-byte core matrix, conflict
 // free), fence to the async proxy, and one thread issues the chunk's MMAs and commits them to the
 // buffer's mbarrier; the next chunk is expanded into the other buffer while the tensor core runs.
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace gssb {
@@ -24,11 +26,16 @@ namespace {
 
 constexpr int kTcThreads = 256;
 constexpr int kTcWarps = kTcThreads / 32;
-constexpr int kKC = 32;                     // frames per pipeline stage (4 MMA k-steps of 8)
+constexpr int kKC = 32;                     // frames per pipeline stage (4 MMA k-steps of 8); = 4 * kTcWarps
 constexpr int kCoreWords = 32;              // one core matrix: 8 rows x 16 bytes
-constexpr int kKCores = kKC / 4;            // core matrices along K per row group
+constexpr int kKCores = kKC / 4;            // core matrices along K per row group (= kTcWarps)
+constexpr int kLook = 8;                    // look-ahead frames read by the padded rows
+constexpr int kAccPerThread = 112;          // register accumulators per thread: NCT <= 224 columns / 2 halves
 
-__host__ __device__ inline int tc_rows(int km, int M) { return ((2 * km + 2 * M + 15) / 16) * 16; }      // NR
+// Row layout of the staged operand S (each block padded to a multiple of 8 rows so that a row group is
+// homogeneous): [Re a (KMP)] [Im a (KMP)] [Re y (8)] [Im y (8)] [zero pad to a multiple of 16].
+__host__ __device__ inline int tc_kmp(int km) { return (km + 7) & ~7; }
+__host__ __device__ inline int tc_rows(int km, int M) { return ((2 * tc_kmp(km) + 16 + 15) / 16) * 16; }  // NR
 __host__ __device__ inline int tc_buf_rows(int km, int M) { return tc_rows(km, M) < 128 ? 128 : tc_rows(km, M); }
 __host__ __device__ inline int tc_n2(int km, int M) { return tc_rows(km, M) > 128 ? tc_rows(km, M) - 128 : 0; }
 __host__ __device__ inline int tc_cols(int km, int M) { return tc_rows(km, M) + tc_n2(km, M); }         // D1 | D2
@@ -86,23 +93,25 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 }  // namespace
 
 template <int M>
-__global__ void __launch_bounds__(kTcThreads, 2) wpe_gram_tc_kernel(WpeArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const SegDev sd = a.segs[blockIdx.y];
   if (!sd.wpe_active) return;
   const int f = blockIdx.x;
-  const int taps = a.taps, km = taps * M, H = a.delay + taps - 1;
+  const int taps = a.taps, km = taps * M, H = a.delay + taps - 1, KMP = tc_kmp(km);
   const int NR = tc_rows(km, M), NB = tc_buf_rows(km, M), N2 = tc_n2(km, M), NCT = NR + N2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int SF = kKC + H + kLook;  // slab frames per chunk
 
   // shared memory carve-up
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);             // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + 16);
-  float2* slab = reinterpret_cast<float2*>(smem_raw + 128);           // (kKC + H) frames x M
-  float* sqw = reinterpret_cast<float*>(slab + (kKC + H) * M);        // kKC
-  const int buf_words = NB * kKC;                                     // one operand buffer (hi or lo)
-  size_t off = 128 + sizeof(float2) * (size_t)(kKC + H) * M + sizeof(float) * kKC;
+  float* wbuf = reinterpret_cast<float*>(smem_raw + 128);             // [2][kKC] Gram weights
+  float* planes = wbuf + 2 * kKC;                                     // [2 stages][re, im][SF * M]
+  const int plane_words = SF * M;
+  size_t off = 128 + sizeof(float) * (2 * kKC + 4 * (size_t)plane_words);
   off = (off + 127) & ~(size_t)127;
+  const int buf_words = NB * kKC;                                     // one operand buffer (hi or lo)
   float* opbuf = reinterpret_cast<float*>(smem_raw + off);            // [stage][hi/lo][buf_words]
 
   if (tid == 0) {
@@ -110,11 +119,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) wpe_gram_tc_kernel(WpeArgs a) {
     mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  uint32_t tmem_cols = 32;
-  while ((int)tmem_cols < NCT) tmem_cols <<= 1;
+  // two accumulator sets (D1 | D2 each) so that a chunk's products start from zero and are folded into
+  // FP32 registers with round-to-nearest: the tensor core's own accumulation truncates, and a chain of
+  // thousands of MMAs would lose ~1e-4 of the Gram
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(tmem_cols)
+                 "r"(512u)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -129,114 +139,158 @@ __global__ void __launch_bounds__(kTcThreads, 2) wpe_gram_tc_kernel(WpeArgs a) {
   const uint32_t sbo = kKCores * 128, lbo = 128;
   const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16);
 
+  // slab of chunk c: frames [c*kKC - H, c*kKC + kKC + kLook), planar, zero outside [0, T) (wpe.hpp:74-75)
+  auto issue_slab = [&](int c, int st) {
+    float* re = planes + (size_t)(2 * st) * plane_words;
+    float* im = re + plane_words;
+    const int t_first = c * kKC - H;
+    for (int i = tid; i < plane_words; i += kTcThreads) {
+      const int fr = i / M;
+      const int t = t_first + fr;
+      if (t >= 0 && t < sd.T) {
+        const float* src = reinterpret_cast<const float*>(yf + (long long)t * M + (i - fr * M));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(re + i)), "l"(src) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(im + i)), "l"(src + 1) : "memory");
+      } else {
+        re[i] = 0.f;
+        im[i] = 0.f;
+      }
+    }
+    if (tid < kKC) {
+      const int t = c * kKC + tid;
+      if (t < sd.T)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wbuf + st * kKC + tid)), "l"(wf + t)
+                     : "memory");
+      else
+        wbuf[st * kKC + tid] = 0.f;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  // register accumulators: thread (quarter q = warp % 4, half h = warp / 4) owns row 32 q + lane and the
+  // columns [h * NCH, (h + 1) * NCH) of D1 | D2
+  const int NCH = NCT / 2;  // NCT is a multiple of 16, NCH of 8
+  float acc[kAccPerThread];
+#pragma unroll
+  for (int i = 0; i < kAccPerThread; ++i) acc[i] = 0.f;
+  const int q = warp & 3, hcol = (warp >> 2) * NCH;
+
+  auto drain = [&](int set) {
+    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(set * 256 + hcol);
+#pragma unroll
+    for (int j = 0; j < kAccPerThread / 8; ++j) {
+      if (j * 8 < NCH) {  // warp-uniform
+        uint32_t v[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(taddr + j * 8)
+                     : "memory");
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[j * 8 + i] += __uint_as_float(v[i]);
+      }
+    }
+  };
+
+  issue_slab(0, 0);
   for (int c = 0; c < nchunk; ++c) {
     const int b = c & 1;
-    const int t0 = c * kKC;
-    if (c >= 2) mbar_wait(&mbar[b], (uint32_t)((c / 2 - 1) & 1));  // MMAs of chunk c-2 released this buffer
-    // slab: frames [t0 - H, t0 + kKC), zero outside [0, T) (wpe.hpp:74-75); sqrt of the Gram weights
-    for (int i = tid; i < (kKC + H) * M; i += kTcThreads) {
-      const int fr = i / M;
-      const int t = t0 - H + fr;
-      slab[i] = (t >= 0 && t < sd.T) ? yf[(long long)t * M + (i - fr * M)] : make_float2(0.f, 0.f);
+    if (c + 1 < nchunk) {
+      issue_slab(c + 1, b ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-    if (tid < kKC) sqw[tid] = t0 + tid < sd.T ? sqrtf(wf[t0 + tid]) : 0.f;
-    __syncthreads();
-    // expand: core matrix (row group rg, k chunk kc) <- lane (row rg*8 + lane/4, frame kc*4 + lane%4)
+    if (c >= 2) {
+      // MMAs of chunk c-2 are complete: operand buffer b and accumulator set b are ours again
+      mbar_wait(&mbar[b], (uint32_t)((c / 2 - 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      drain(b);
+    }
+    __syncthreads();  // slab of chunk c has landed for everyone
+    // expand: warp w owns k chunk w (frames 4w .. 4w+3), lane -> (row rg*8 + lane/4, frame 4w + lane%4);
+    // a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
+    const float* re = planes + (size_t)(2 * b) * plane_words;
+    const float* im = re + plane_words;
     float* hi_buf = opbuf + (size_t)(2 * b) * buf_words;
     float* lo_buf = hi_buf + buf_words;
-    const int ncores = (NB / 8) * kKCores;
-    for (int core = warp; core < ncores; core += kTcWarps) {
-      const int rg = core / kKCores, kc = core - rg * kKCores;
-      const int r = rg * 8 + (lane >> 2), k = kc * 4 + (lane & 3);
-      float v = 0.f;
-      if (r < 2 * km) {
-        const int e = r < km ? r : r - km;
-        const float2 y = slab[(k + e / M) * M + e % M];
-        v = r < km ? y.x : y.y;
-      } else if (r < 2 * km + 2 * M) {
-        const int cc = r - 2 * km;
-        const float2 y = slab[(k + H) * M + (cc < M ? cc : cc - M)];
-        v = cc < M ? y.x : y.y;
-      }
-      v *= sqw[k];
+    const int k = warp * 4 + (lane & 3), r8 = lane >> 2;
+    const float sq = sqrtf(wbuf[b * kKC + k]);
+    const int word0 = warp * kCoreWords + lane;  // core (rg, kc = warp) -> (rg * kKCores + warp) * 32 + lane
+    const int nrg_a = KMP / 8;
+    auto put = [&](int rg, float v) {
+      v *= sq;
       const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-      hi_buf[core * kCoreWords + lane] = hi;
-      lo_buf[core * kCoreWords + lane] = v - hi;
+      hi_buf[rg * (kKCores * kCoreWords) + word0] = hi;
+      lo_buf[rg * (kKCores * kCoreWords) + word0] = v - hi;
+    };
+    for (int rg = 0; rg < nrg_a; ++rg) {  // history window: element e = rg*8 + r8 of frame k is slab[k*M + e]
+      put(rg, re[k * M + rg * 8 + r8]);
+      put(nrg_a + rg, im[k * M + rg * 8 + r8]);
     }
+    put(2 * nrg_a, re[(k + H) * M + r8]);      // current frame (rows >= M of the block are never read back)
+    put(2 * nrg_a + 1, im[(k + H) * M + r8]);
+    for (int rg = 2 * nrg_a + 2; rg < NB / 8; ++rg) put(rg, 0.f);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core reads
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a_hi = smem_u32(hi_buf), a_lo = smem_u32(lo_buf);
+      const uint32_t d1 = tmem_base + (uint32_t)(b * 256), d2 = d1 + (uint32_t)NR;
 #pragma unroll
       for (int ks = 0; ks < kKC / 8; ++ks) {
-        const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
-        const uint32_t ko = ks * 256;  // two core matrices along K per MMA
+        const uint32_t accf = ks > 0 ? 1u : 0u;  // every chunk starts its accumulator set from zero
+        const uint32_t ko = ks * 256;            // two core matrices along K per MMA
         const uint64_t dh = make_smem_desc(a_hi + ko, lbo, sbo), dl = make_smem_desc(a_lo + ko, lbo, sbo);
-        mma_tf32(tmem_base, dh, dh, idesc1, acc);
-        mma_tf32(tmem_base, dh, dl, idesc1, 1u);
-        mma_tf32(tmem_base, dl, dh, idesc1, 1u);
+        mma_tf32(d1, dh, dh, idesc1, accf);
+        mma_tf32(d1, dh, dl, idesc1, 1u);
+        mma_tf32(d1, dl, dh, idesc1, 1u);
         if (N2 > 0) {
           const uint32_t ra = ((NR - 128) / 8) * sbo, rb = 16 * sbo;  // rows NR-128.. and rows 128..
           const uint64_t ah = make_smem_desc(a_hi + ra + ko, lbo, sbo), al = make_smem_desc(a_lo + ra + ko, lbo, sbo);
           const uint64_t bh = make_smem_desc(a_hi + rb + ko, lbo, sbo), bl = make_smem_desc(a_lo + rb + ko, lbo, sbo);
-          mma_tf32(tmem_base + NR, ah, bh, idesc2, acc);
-          mma_tf32(tmem_base + NR, ah, bl, idesc2, 1u);
-          mma_tf32(tmem_base + NR, al, bh, idesc2, 1u);
+          mma_tf32(d2, ah, bh, idesc2, accf);
+          mma_tf32(d2, ah, bl, idesc2, 1u);
+          mma_tf32(d2, al, bh, idesc2, 1u);
         }
       }
       tc_commit(&mbar[b]);
     }
-    // no barrier here: the next chunk only touches the slab (free after the sync above) and the other buffer
   }
-  // drain: the last use of each buffer
-  for (int b = 0; b < 2; ++b) {
-    const int uses = (nchunk - b + 1) / 2;
-    if (uses > 0) mbar_wait(&mbar[b], (uint32_t)((uses - 1) & 1));
+  // fold in the last two chunks
+  for (int c = max(0, nchunk - 2); c < nchunk; ++c) {
+    mbar_wait(&mbar[c & 1], (uint32_t)((c / 2) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    drain(c & 1);
   }
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // epilogue: thread i of warps 0..3 owns accumulator row i (tensor-memory lane i)
-  float* out = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT);
-  if (warp < 4) {
-    const int row = warp * 32 + lane;
-    for (int c0 = 0; c0 < NCT; c0 += 16) {
-      uint32_t v[16];
-      const uint32_t taddr = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-          "%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-            "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr)
-          : "memory");
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      float4* o4 = reinterpret_cast<float4*>(out + (long long)row * NCT + c0);
+  float* out = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT) + (long long)(q * 32 + lane) * NCT + hcol;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        o4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
-                            __uint_as_float(v[4 * j + 3]));
-    }
-  }
+  for (int j = 0; j < kAccPerThread / 4; ++j)
+    if (j * 4 < NCH)
+      reinterpret_cast<float4*>(out)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u) : "memory");
   }
 }
 
 // ---------------------------------------------------------------------------
-int wpe_tc_supported(int km, int M) { return tc_rows(km, M) <= 256 && tc_cols(km, M) <= 512 ? 1 : 0; }
+int wpe_tc_supported(int km, int M) { return tc_cols(km, M) <= 2 * kAccPerThread ? 1 : 0; }
 int wpe_tc_cell_floats(int km, int M) { return 128 * tc_cols(km, M); }
 int wpe_tc_rows(int km, int M) { return tc_rows(km, M); }
 
 template <int M>
 static cudaError_t launch_tc_m(const WpeArgs& a, int nseg, int F, cudaStream_t st) {
   const int km = a.taps * M, H = a.delay + a.taps - 1;
-  size_t off = 128 + sizeof(float2) * (size_t)(kKC + H) * M + sizeof(float) * kKC;
+  size_t off = 128 + sizeof(float) * (2 * kKC + 4 * (size_t)(kKC + H + kLook) * M);
   off = (off + 127) & ~(size_t)127;
-  const size_t smem = off + sizeof(float) * 4 * (size_t)tc_buf_rows(km, M) * kKC;
-  if (smem > 110 * 1024) return cudaErrorInvalidConfiguration;
+  size_t smem = off + sizeof(float) * 4 * (size_t)tc_buf_rows(km, M) * kKC;
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+  // all 512 tensor-memory columns belong to one CTA: keep a second CTA off the SM
+  smem = std::max<size_t>(smem, 120 * 1024);
   cudaError_t e = cudaFuncSetAttribute(wpe_gram_tc_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   wpe_gram_tc_kernel<M><<<dim3(F, nseg), kTcThreads, smem, st>>>(a);

@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
   if (a.use_tc) {
     // raw real accumulators of the tensor-core Gram (wpe_gram_tc.cu): D1 = S[0..128) S^T (NR columns),
     // D2 = S[NR-128..NR) S[128..NR)^T (N2 columns); G(a,b) by symmetry
-    const int NR = ((2 * km + 2 * M + 15) / 16) * 16, N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
+    // operand rows: [Re a (KMP)] [Im a (KMP)] [Re y (8)] [Im y (8)], KMP = km rounded up to 8
+    const int KMP = (km + 7) & ~7, NR = ((2 * KMP + 16 + 15) / 16) * 16, N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
     const float* raw = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT);
     auto G = [&](int x, int y) -> double {
       if (x < 128) return (double)raw[x * NCT + y];
@@ -283,15 +284,15 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
     for (int idx = tid; idx < km * km; idx += nth) {
       const int i = idx / km, j = idx - i * km;
       if (j > i) continue;
-      const double re = G(i, j) + G(km + i, km + j);
-      const double im = i == j ? 0.0 : G(km + i, j) - G(i, km + j);
+      const double re = G(i, j) + G(KMP + i, KMP + j);
+      const double im = i == j ? 0.0 : G(KMP + i, j) - G(i, KMP + j);
       A[i * ld + j] = cd_make(re, im);
       A[j * ld + i] = cd_make(re, -im);
     }
     for (int idx = tid; idx < km * M; idx += nth) {
       const int i = idx / M, c = idx - i * M;
-      B[i * M + c] = cd_make(G(i, 2 * km + c) + G(km + i, 2 * km + M + c),
-                             G(km + i, 2 * km + c) - G(i, 2 * km + M + c));
+      B[i * M + c] = cd_make(G(i, 2 * KMP + c) + G(KMP + i, 2 * KMP + 8 + c),
+                             G(KMP + i, 2 * KMP + c) - G(i, 2 * KMP + 8 + c));
     }
   } else {
   // lower triangle of R (upper mirrored by hermitize) and P, summed over chunks in double
