@@ -24,8 +24,8 @@ namespace gssb {
 
 namespace {
 
-constexpr int kTcThreads = 256;
-constexpr int kTcWarps = kTcThreads / 32;
+constexpr int kTcWorkers = 256;             // 8 warps expand the operands and fold the accumulators
+constexpr int kTcThreads = kTcWorkers + 32; // + one warp whose lane 0 issues the MMAs
 constexpr int kKC = 32;                     // frames per pipeline stage (4 MMA k-steps of 8); = 4 * kTcWarps
 constexpr int kCoreWords = 32;              // one core matrix: 8 rows x 16 bytes
 constexpr int kKCores = kKC / 4;            // core matrices along K per row group (= kTcWarps)
@@ -85,6 +85,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void workers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kTcWorkers) : "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -104,25 +108,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   const int SF = kKC + H + kLook;  // slab frames per chunk
 
   // shared memory carve-up
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);             // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + 16);
-  float* wbuf = reinterpret_cast<float*>(smem_raw + 128);             // [2][kKC] Gram weights
-  float* planes = wbuf + 2 * kKC;                                     // [2 stages][re, im][SF * M]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);             // [2] operands of a chunk are staged
+  uint64_t* done = full + 2;                                          // [2] MMAs of a chunk are complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + 32);
+  float* wbuf = reinterpret_cast<float*>(smem_raw + 128);             // [3][kKC] Gram weights
+  float* planes = wbuf + 3 * kKC;                                     // [3 stages][re, im][SF * M]
   const int plane_words = SF * M;
-  size_t off = 128 + sizeof(float) * (2 * kKC + 4 * (size_t)plane_words);
+  size_t off = 128 + sizeof(float) * (3 * kKC + 6 * (size_t)plane_words);
   off = (off + 127) & ~(size_t)127;
   const int buf_words = NB * kKC;                                     // one operand buffer (hi or lo)
   float* opbuf = reinterpret_cast<float*>(smem_raw + off);            // [stage][hi/lo][buf_words]
 
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    mbar_init(&full[0], kTcWorkers / 32);
+    mbar_init(&full[1], kTcWorkers / 32);
+    mbar_init(&done[0], 1);
+    mbar_init(&done[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // two accumulator sets (D1 | D2 each) so that a chunk's products start from zero and are folded into
-  // FP32 registers with round-to-nearest: the tensor core's own accumulation truncates, and a chain of
-  // thousands of MMAs would lose ~1e-4 of the Gram
-  if (warp == 0) {
+  // Two accumulator sets (D1 | D2 each): every chunk's products start from zero and are folded into FP32
+  // registers with round-to-nearest. The tensor core's own accumulation truncates; a chain of thousands
+  // of MMAs loses ~1e-4 of the Gram, a chain of 12 stays at the 3xTF32 level (1e-6).
+  if (warp == kTcWorkers / 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512u)
                  : "memory");
@@ -132,147 +139,170 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
-
-  const float2* yf = a.yobs + sd.y_off + (long long)f * sd.T * M;
-  const float* wf = a.w + sd.w_off + (long long)f * sd.T;
   const int nchunk = (sd.T + kKC - 1) / kKC;
   const uint32_t sbo = kKCores * 128, lbo = 128;
-  const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16);
 
-  // slab of chunk c: frames [c*kKC - H, c*kKC + kKC + kLook), planar, zero outside [0, T) (wpe.hpp:74-75)
-  auto issue_slab = [&](int c, int st) {
-    float* re = planes + (size_t)(2 * st) * plane_words;
-    float* im = re + plane_words;
-    const int t_first = c * kKC - H;
-    for (int i = tid; i < plane_words; i += kTcThreads) {
-      const int fr = i / M;
-      const int t = t_first + fr;
-      if (t >= 0 && t < sd.T) {
-        const float* src = reinterpret_cast<const float*>(yf + (long long)t * M + (i - fr * M));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(re + i)), "l"(src) : "memory");
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(im + i)), "l"(src + 1) : "memory");
-      } else {
-        re[i] = 0.f;
-        im[i] = 0.f;
+  if (warp == kTcWorkers / 32) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16);
+      for (int c = 0; c < nchunk; ++c) {
+        const int b = c & 1;
+        mbar_wait(&full[b], (uint32_t)((c / 2) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a_hi = smem_u32(opbuf + (size_t)(2 * b) * buf_words), a_lo = a_hi + 4u * (uint32_t)buf_words;
+        const uint32_t d1 = tmem_base + (uint32_t)(b * 256), d2 = d1 + (uint32_t)NR;
+#pragma unroll
+        for (int ks = 0; ks < kKC / 8; ++ks) {
+          const uint32_t accf = ks > 0 ? 1u : 0u;  // every chunk starts its accumulator set from zero
+          const uint32_t ko = ks * 256;            // two core matrices along K per MMA
+          const uint64_t dh = make_smem_desc(a_hi + ko, lbo, sbo), dl = make_smem_desc(a_lo + ko, lbo, sbo);
+          mma_tf32(d1, dh, dh, idesc1, accf);
+          mma_tf32(d1, dh, dl, idesc1, 1u);
+          mma_tf32(d1, dl, dh, idesc1, 1u);
+          if (N2 > 0) {
+            const uint32_t ra = ((NR - 128) / 8) * sbo, rb = 16 * sbo;  // rows NR-128.. and rows 128..
+            const uint64_t ah = make_smem_desc(a_hi + ra + ko, lbo, sbo), al = make_smem_desc(a_lo + ra + ko, lbo, sbo);
+            const uint64_t bh = make_smem_desc(a_hi + rb + ko, lbo, sbo), bl = make_smem_desc(a_lo + rb + ko, lbo, sbo);
+            mma_tf32(d2, ah, bh, idesc2, accf);
+            mma_tf32(d2, ah, bl, idesc2, 1u);
+            mma_tf32(d2, al, bh, idesc2, 1u);
+          }
+        }
+        tc_commit(&done[b]);
       }
     }
-    if (tid < kKC) {
-      const int t = c * kKC + tid;
-      if (t < sd.T)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wbuf + st * kKC + tid)), "l"(wf + t)
-                     : "memory");
-      else
-        wbuf[st * kKC + tid] = 0.f;
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-
-  // register accumulators: thread (quarter q = warp % 4, half h = warp / 4) owns row 32 q + lane and the
-  // columns [h * NCH, (h + 1) * NCH) of D1 | D2
-  const int NCH = NCT / 2;  // NCT is a multiple of 16, NCH of 8
-  float acc[kAccPerThread];
-#pragma unroll
-  for (int i = 0; i < kAccPerThread; ++i) acc[i] = 0.f;
-  const int q = warp & 3, hcol = (warp >> 2) * NCH;
-
-  auto drain = [&](int set) {
-    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(set * 256 + hcol);
-#pragma unroll
-    for (int j = 0; j < kAccPerThread / 8; ++j) {
-      if (j * 8 < NCH) {  // warp-uniform
-        uint32_t v[8];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                     : "r"(taddr + j * 8)
-                     : "memory");
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[j * 8 + i] += __uint_as_float(v[i]);
-      }
-    }
-  };
-
-  issue_slab(0, 0);
-  for (int c = 0; c < nchunk; ++c) {
-    const int b = c & 1;
-    if (c + 1 < nchunk) {
-      issue_slab(c + 1, b ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    if (c >= 2) {
-      // MMAs of chunk c-2 are complete: operand buffer b and accumulator set b are ours again
-      mbar_wait(&mbar[b], (uint32_t)((c / 2 - 1) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      drain(b);
-    }
-    __syncthreads();  // slab of chunk c has landed for everyone
-    // expand: warp w owns k chunk w (frames 4w .. 4w+3), lane -> (row rg*8 + lane/4, frame 4w + lane%4);
-    // a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
-    const float* re = planes + (size_t)(2 * b) * plane_words;
-    const float* im = re + plane_words;
-    float* hi_buf = opbuf + (size_t)(2 * b) * buf_words;
-    float* lo_buf = hi_buf + buf_words;
-    const int k = warp * 4 + (lane & 3), r8 = lane >> 2;
-    const float sq = sqrtf(wbuf[b * kKC + k]);
-    const int word0 = warp * kCoreWords + lane;  // core (rg, kc = warp) -> (rg * kKCores + warp) * 32 + lane
-    const int nrg_a = KMP / 8;
-    auto put = [&](int rg, float v) {
-      v *= sq;
-      const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-      hi_buf[rg * (kKCores * kCoreWords) + word0] = hi;
-      lo_buf[rg * (kKCores * kCoreWords) + word0] = v - hi;
-    };
-    for (int rg = 0; rg < nrg_a; ++rg) {  // history window: element e = rg*8 + r8 of frame k is slab[k*M + e]
-      put(rg, re[k * M + rg * 8 + r8]);
-      put(nrg_a + rg, im[k * M + rg * 8 + r8]);
-    }
-    put(2 * nrg_a, re[(k + H) * M + r8]);      // current frame (rows >= M of the block are never read back)
-    put(2 * nrg_a + 1, im[(k + H) * M + r8]);
-    for (int rg = 2 * nrg_a + 2; rg < NB / 8; ++rg) put(rg, 0.f);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core reads
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a_hi = smem_u32(hi_buf), a_lo = smem_u32(lo_buf);
-      const uint32_t d1 = tmem_base + (uint32_t)(b * 256), d2 = d1 + (uint32_t)NR;
-#pragma unroll
-      for (int ks = 0; ks < kKC / 8; ++ks) {
-        const uint32_t accf = ks > 0 ? 1u : 0u;  // every chunk starts its accumulator set from zero
-        const uint32_t ko = ks * 256;            // two core matrices along K per MMA
-        const uint64_t dh = make_smem_desc(a_hi + ko, lbo, sbo), dl = make_smem_desc(a_lo + ko, lbo, sbo);
-        mma_tf32(d1, dh, dh, idesc1, accf);
-        mma_tf32(d1, dh, dl, idesc1, 1u);
-        mma_tf32(d1, dl, dh, idesc1, 1u);
-        if (N2 > 0) {
-          const uint32_t ra = ((NR - 128) / 8) * sbo, rb = 16 * sbo;  // rows NR-128.. and rows 128..
-          const uint64_t ah = make_smem_desc(a_hi + ra + ko, lbo, sbo), al = make_smem_desc(a_lo + ra + ko, lbo, sbo);
-          const uint64_t bh = make_smem_desc(a_hi + rb + ko, lbo, sbo), bl = make_smem_desc(a_lo + rb + ko, lbo, sbo);
-          mma_tf32(d2, ah, bh, idesc2, accf);
-          mma_tf32(d2, ah, bl, idesc2, 1u);
-          mma_tf32(d2, al, bh, idesc2, 1u);
+  } else {
+    // ===== workers: stage the slab, expand it into MMA operands, fold finished accumulators =====
+    const float2* yf = a.yobs + sd.y_off + (long long)f * sd.T * M;
+    const float* wf = a.w + sd.w_off + (long long)f * sd.T;
+    // slab of chunk c: frames [c*kKC - H, c*kKC + kKC + kLook), planar, zero outside [0, T) (wpe.hpp:74-75)
+    auto issue_slab = [&](int c) {
+      const int st = c % 3;
+      float* re = planes + (size_t)(2 * st) * plane_words;
+      float* im = re + plane_words;
+      const int t_first = c * kKC - H;
+      for (int i = tid; i < plane_words; i += kTcWorkers) {
+        const int fr = i / M;
+        const int t = t_first + fr;
+        if (t >= 0 && t < sd.T) {
+          const float* src = reinterpret_cast<const float*>(yf + (long long)t * M + (i - fr * M));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(re + i)), "l"(src) : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(im + i)), "l"(src + 1) : "memory");
+        } else {
+          re[i] = 0.f;
+          im[i] = 0.f;
         }
       }
-      tc_commit(&mbar[b]);
-    }
-  }
-  // fold in the last two chunks
-  for (int c = max(0, nchunk - 2); c < nchunk; ++c) {
-    mbar_wait(&mbar[c & 1], (uint32_t)((c / 2) & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    drain(c & 1);
-  }
+      if (tid < kKC) {
+        const int t = c * kKC + tid;
+        if (t < sd.T)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wbuf + st * kKC + tid)), "l"(wf + t)
+                       : "memory");
+        else
+          wbuf[st * kKC + tid] = 0.f;
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 
-  float* out = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT) + (long long)(q * 32 + lane) * NCT + hcol;
+    // register accumulators: thread (quarter q = warp % 4, half h = warp / 4) owns row 32 q + lane and the
+    // columns [h * NCH, (h + 1) * NCH) of D1 | D2
+    const int NCH = NCT / 2;  // NCT is a multiple of 16, NCH of 8
+    float acc[kAccPerThread];
 #pragma unroll
-  for (int j = 0; j < kAccPerThread / 4; ++j)
-    if (j * 4 < NCH)
-      reinterpret_cast<float4*>(out)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    for (int i = 0; i < kAccPerThread; ++i) acc[i] = 0.f;
+    const int q = warp & 3, hcol = (warp >> 2) * NCH;
+
+    auto drain = [&](int set) {
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(set * 256 + hcol);
+      constexpr int kBatch = 32;  // columns in flight per wait
+#pragma unroll
+      for (int b0 = 0; b0 < kAccPerThread; b0 += kBatch) {
+        uint32_t v[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch / 8; ++j) {
+          const int col = b0 + j * 8;
+          if (col < kAccPerThread && col < NCH)  // warp-uniform
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=r"(v[j * 8]), "=r"(v[j * 8 + 1]), "=r"(v[j * 8 + 2]), "=r"(v[j * 8 + 3]),
+                           "=r"(v[j * 8 + 4]), "=r"(v[j * 8 + 5]), "=r"(v[j * 8 + 6]), "=r"(v[j * 8 + 7])
+                         : "r"(taddr + col)
+                         : "memory");
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < kBatch / 8; ++j) {
+          const int col = b0 + j * 8;
+          if (col < kAccPerThread && col < NCH) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[col + i] += __uint_as_float(v[j * 8 + i]);
+          }
+        }
+      }
+    };
+
+    issue_slab(0);
+    for (int c = 0; c < nchunk; ++c) {
+      const int b = c & 1, st = c % 3;
+      if (c + 1 < nchunk) {
+        issue_slab(c + 1);  // stage (c+1)%3 was last read by the expansion of chunk c-2
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      workers_sync();  // slab of chunk c has landed for every worker
+      if (c >= 2) {
+        // MMAs of chunk c-2 are complete: operand buffer b and accumulator set b are ours again
+        mbar_wait(&done[b], (uint32_t)((c / 2 - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        drain(b);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      }
+      // expand: warp w owns k chunk w (frames 4w .. 4w+3), lane -> (row rg*8 + lane/4, frame 4w + lane%4);
+      // a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
+      const float* re = planes + (size_t)(2 * st) * plane_words;
+      const float* im = re + plane_words;
+      float* hi_buf = opbuf + (size_t)(2 * b) * buf_words;
+      float* lo_buf = hi_buf + buf_words;
+      const int k = warp * 4 + (lane & 3), r8 = lane >> 2;
+      const float sq = sqrtf(wbuf[st * kKC + k]);
+      const int word0 = warp * kCoreWords + lane;  // core (rg, kc = warp) -> (rg * kKCores + warp) * 32 + lane
+      const int nrg_a = KMP / 8;
+      auto put = [&](int rg, float v) {
+        v *= sq;
+        const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+        hi_buf[rg * (kKCores * kCoreWords) + word0] = hi;
+        lo_buf[rg * (kKCores * kCoreWords) + word0] = v - hi;
+      };
+#pragma unroll 5
+      for (int rg = 0; rg < nrg_a; ++rg) {  // history window: element e = rg*8 + r8 of frame k is slab[k*M + e]
+        put(rg, re[k * M + rg * 8 + r8]);
+        put(nrg_a + rg, im[k * M + rg * 8 + r8]);
+      }
+      put(2 * nrg_a, re[(k + H) * M + r8]);      // current frame (rows >= M of the block are never read back)
+      put(2 * nrg_a + 1, im[(k + H) * M + r8]);
+      for (int rg = 2 * nrg_a + 2; rg < NB / 8; ++rg) put(rg, 0.f);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[b]);
+    }
+    // fold in the last two chunks
+    for (int c = max(0, nchunk - 2); c < nchunk; ++c) {
+      mbar_wait(&done[c & 1], (uint32_t)((c / 2) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      drain(c & 1);
+    }
+    float* out = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT) +
+                 (long long)(q * 32 + lane) * NCT + hcol;
+#pragma unroll
+    for (int j = 0; j < kAccPerThread / 4; ++j)
+      if (j * 4 < NCH)
+        reinterpret_cast<float4*>(out)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
   __syncthreads();
-  if (warp == 0) {
+  if (warp == kTcWorkers / 32) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u) : "memory");
   }
 }
@@ -285,7 +315,7 @@ int wpe_tc_rows(int km, int M) { return tc_rows(km, M); }
 template <int M>
 static cudaError_t launch_tc_m(const WpeArgs& a, int nseg, int F, cudaStream_t st) {
   const int km = a.taps * M, H = a.delay + a.taps - 1;
-  size_t off = 128 + sizeof(float) * (2 * kKC + 4 * (size_t)(kKC + H + kLook) * M);
+  size_t off = 128 + sizeof(float) * (3 * kKC + 6 * (size_t)(kKC + H + kLook) * M);
   off = (off + 127) & ~(size_t)127;
   size_t smem = off + sizeof(float) * 4 * (size_t)tc_buf_rows(km, M) * kKC;
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;

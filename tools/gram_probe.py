@@ -34,7 +34,7 @@ def main():
     ctx = gss.default_context()
     lib = capi.load()
     for (f, t, m, taps, delay) in [(3, 200, 7, 10, 2), (2, 333, 8, 10, 3), (2, 100, 2, 5, 1), (2, 150, 4, 8, 2),
-                                   (2, 64, 1, 4, 2), (2, 97, 5, 10, 2)]:
+                                   (2, 64, 1, 4, 2), (2, 97, 5, 10, 2), (513, 79, 3, 10, 2), (4, 5001, 7, 10, 2)]:
         rng = np.random.RandomState(t)
         y = (rng.randn(f, t, m) + 1j * rng.randn(f, t, m)).astype(np.complex64)
         y[:, 3:] += 0.6 * y[:, :-3]
