@@ -99,6 +99,7 @@ struct KClock {
     if (b) cudaEventRecord(b, c->stream);
   }
 };
+constexpr int kWpeFallbackSlots = 8;  // concurrent eigenvalue-floor repairs per WPE launch; more is a loud error
 enum KernelId { kK_stft = 0, kK_wpe_power, kK_wpe_gram, kK_wpe_solve, kK_wpe_apply, kK_em_pass, kK_em_update,
                 kK_mvdr, kK_apply, kK_istft, kK_misc };
 
@@ -254,6 +255,8 @@ struct Group {
   float2 *gram = nullptr, *gconj = nullptr;
   float* gram_raw = nullptr;
   int use_tc = 0;
+  cdbl* fb_scratch = nullptr;
+  int* fb_ticket = nullptr;
   status_t* status = nullptr;
   int *ref = nullptr, *zeroed = nullptr;
   long long tot_audio = 0, tot_y = 0, tot_g = 0, tot_x = 0, tot_wave = 0, tot_pat = 0, tot_mask = 0;
@@ -412,6 +415,8 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
     else
       g.gram = m.get<float2>((size_t)o_wcell * wcell);
     g.gconj = m.get<float2>(o_gw);
+    g.fb_scratch = m.get<cdbl>((size_t)kWpeFallbackSlots * wpe_fallback_slot_elems(km, M));
+    g.fb_ticket = m.get<int>(1);
   }
   if (m.last != cudaSuccess) {
     const std::string why = std::string("device allocation failed: ") + cudaGetErrorString(m.last);
@@ -454,6 +459,9 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
   a.debug_rp = nullptr;
+  a.fb_scratch = g.fb_scratch;
+  a.fb_ticket = g.fb_ticket;
+  a.fb_slots = kWpeFallbackSlots;
   a.gconj = g.gconj;
   a.segs = g.d_segs;
   a.status = g.status;
@@ -464,6 +472,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
   a.psd_context = w.psd_context;
   for (int it = 0; it < w.iterations; ++it) {
     a.ycur = it == 0 ? g.Y : g.Yd;
+    CU_TRY(c, cudaMemsetAsync(g.fb_ticket, 0, sizeof(int), c->stream));
     for (int step = 0; step < 4; ++step) {
       KClock k(c, kK_wpe_power + step);
       CU_TRY(c, launch_wpe_step(step, a, g.nseg, g.F, g.max_T, g.max_wchunks, c->stream));
@@ -495,6 +504,7 @@ gss_status run_em(gss_b200_ctx* c, Group& g, const EmRun& r) {
   u.ck = g.ck;
   u.bin_ll = g.bin_ll;
   u.status = g.status;
+  u.c0 = -(double)g.M * std::log(2.0 * M_PI) + std::lgamma((double)g.M);
   u.cell_stride = g.cell_stride;
   u.F = g.F;
   u.mode = r.from_state ? kEmFromState : kEmInit;
@@ -1271,6 +1281,9 @@ gss_status gss_b200_debug_wpe_gram(gss_b200_ctx* c, const float* in, int32_t bin
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
   a.debug_rp = d_rp;
+  a.fb_scratch = g.fb_scratch;
+  a.fb_ticket = g.fb_ticket;
+  a.fb_slots = 0;
   a.gconj = g.gconj;
   a.segs = g.d_segs;
   a.status = g.status;

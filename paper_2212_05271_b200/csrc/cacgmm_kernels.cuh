@@ -530,9 +530,11 @@ __global__ void __launch_bounds__(KT * 32) em_update_kernel(EmUpdateArgs a) {
       for (int e = lane; e < MM; e += 32) F[e] = B[e];
       __syncwarp();
       if (warp_cholesky<M>(F, lane)) {
-        double ld = 0.0;
-        for (int i = 0; i < M; ++i) ld += log(F[i * M + i].re);
-        my_ld = 2.0 * ld;
+        // log|B| = 2 sum log L_ii; B is trace-normalised to M, so the product of the (<= 8) pivots cannot
+        // overflow and one logarithm replaces M of them
+        double pd = 1.0;
+        for (int i = 0; i < M; ++i) pd *= F[i * M + i].re;
+        my_ld = 2.0 * log(pd);
         warp_cholesky_inverse<M>(F, inv, lane);
       } else {
         // rare path, one lane: eigenvalue-floor fallback, then the retry on regularize(B)
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(KT * 32) em_update_kernel(EmUpdateArgs a) {
 
   // E-step constants per activity pattern (cacgmm.hpp:196-237):
   //   ck = lp + c0 - log|B_k|, lp = log max(1e-10, pi_k) - log z, z = sum of active pi
-  const double c0 = -(double)M * log(2.0 * 3.14159265358979323846) + lgamma((double)M);
+  const double c0 = a.c0;  // -M log(2 pi) + lgamma(M), from the host
   float* tab = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
   for (int idx = threadIdx.x; idx < sd.npat * KT; idx += KT * 32) {
     const int p = idx / KT, kk = idx - p * KT;

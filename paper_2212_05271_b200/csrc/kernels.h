@@ -49,9 +49,14 @@ struct WpeArgs {
   status_t* status;
   double regularization;
   int M, taps, delay, psd_context;
+  cdbl* fb_scratch;     // eigenvalue-floor fallback: fb_slots slots of wpe_fallback_slot_elems cdbl
+  int* fb_ticket;
+  int fb_slots;
   cdbl* debug_rp;       // non-null: the solve kernel only dumps hermitized R (km x km) and P (km x M) per bin
   int use_tc;           // 1: the Gram of this iteration came from wpe_gram_tc_kernel
 };
+/// cdbl elements of one scratch slot of the WPE solve's eigenvalue-floor fallback: A, two work matrices, B, eigenvalues
+__host__ __device__ inline int wpe_fallback_slot_elems(int km, int M) { return 3 * km * km + km * M + km / 2 + 1; }
 /// cfloat elements of one (segment, bin, chunk) Gram cell
 int wpe_gram_cell_elems(int km, int M);
 /// tensor-core Gram (wpe_gram_tc.cu)
@@ -92,6 +97,7 @@ struct EmUpdateArgs {
   float* ck;
   double* bin_ll;   // (f) slot of this sweep
   status_t* status; // per segment of the group
+  double c0;        // -M log(2 pi) + lgamma(M) (cacgmm.hpp:196)
   int cell_stride;
   int mode;
   int F;

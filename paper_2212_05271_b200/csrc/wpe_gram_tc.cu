@@ -24,13 +24,14 @@ namespace gssb {
 
 namespace {
 
-constexpr int kTcWorkers = 256;             // 8 warps expand the operands and fold the accumulators
+constexpr int kTcWorkers = 512;             // 16 warps expand the operands and fold the accumulators
+constexpr int kTcWorkerWarps = kTcWorkers / 32;
 constexpr int kTcThreads = kTcWorkers + 32; // + one warp whose lane 0 issues the MMAs
 constexpr int kKC = 32;                     // frames per pipeline stage (4 MMA k-steps of 8); = 4 * kTcWarps
 constexpr int kCoreWords = 32;              // one core matrix: 8 rows x 16 bytes
 constexpr int kKCores = kKC / 4;            // core matrices along K per row group (= kTcWarps)
 constexpr int kLook = 8;                    // look-ahead frames read by the padded rows
-constexpr int kAccPerThread = 112;          // register accumulators per thread: NCT <= 224 columns / 2 halves
+constexpr int kAccPerThread = 56;           // register accumulators per thread: NCT <= 224 columns / 4 quarters
 
 // Row layout of the staged operand S (each block padded to a multiple of 8 rows so that a row group is
 // homogeneous): [Re a (KMP)] [Im a (KMP)] [Re y (8)] [Im y (8)] [zero pad to a multiple of 16].
@@ -89,6 +90,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void workers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kTcWorkers) : "memory"); }
+__device__ __forceinline__ float sqrt_approx_tc(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -96,13 +102,16 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 
 }  // namespace
 
-template <int M>
+/// TAPS > 0 fixes the tap count at compile time (all loops unroll, no guards); TAPS == 0 reads it from the
+/// arguments.
+template <int M, int TAPS>
 __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const SegDev sd = a.segs[blockIdx.y];
   if (!sd.wpe_active) return;
   const int f = blockIdx.x;
-  const int taps = a.taps, km = taps * M, H = a.delay + taps - 1, KMP = tc_kmp(km);
+  const int taps = TAPS > 0 ? TAPS : a.taps;
+  const int km = taps * M, H = a.delay + taps - 1, KMP = tc_kmp(km);
   const int NR = tc_rows(km, M), NB = tc_buf_rows(km, M), N2 = tc_n2(km, M), NCT = NR + N2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int SF = kKC + H + kLook;  // slab frames per chunk
@@ -120,8 +129,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   float* opbuf = reinterpret_cast<float*>(smem_raw + off);            // [stage][hi/lo][buf_words]
 
   if (tid == 0) {
-    mbar_init(&full[0], kTcWorkers / 32);
-    mbar_init(&full[1], kTcWorkers / 32);
+    mbar_init(&full[0], kTcWorkerWarps);
+    mbar_init(&full[1], kTcWorkerWarps);
     mbar_init(&done[0], 1);
     mbar_init(&done[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -129,7 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   // Two accumulator sets (D1 | D2 each): every chunk's products start from zero and are folded into FP32
   // registers with round-to-nearest. The tensor core's own accumulation truncates; a chain of thousands
   // of MMAs loses ~1e-4 of the Gram, a chain of 12 stays at the 3xTF32 level (1e-6).
-  if (warp == kTcWorkers / 32) {
+  if (warp == kTcWorkerWarps) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512u)
                  : "memory");
@@ -142,7 +151,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   const int nchunk = (sd.T + kKC - 1) / kKC;
   const uint32_t sbo = kKCores * 128, lbo = 128;
 
-  if (warp == kTcWorkers / 32) {
+  if (warp == kTcWorkerWarps) {
     // ===== MMA issuer =====
     if (lane == 0) {
       const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16);
@@ -186,7 +195,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
         const int fr = i / M;
         const int t = t_first + fr;
         if (t >= 0 && t < sd.T) {
-          const float* src = reinterpret_cast<const float*>(yf + (long long)t * M + (i - fr * M));
+          const float* src = reinterpret_cast<const float*>(yf + (long long)t_first * M + i);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(re + i)), "l"(src) : "memory");
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(im + i)), "l"(src + 1) : "memory");
         } else {
@@ -205,41 +214,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
-    // register accumulators: thread (quarter q = warp % 4, half h = warp / 4) owns row 32 q + lane and the
-    // columns [h * NCH, (h + 1) * NCH) of D1 | D2
-    const int NCH = NCT / 2;  // NCT is a multiple of 16, NCH of 8
+    // register accumulators: thread (lane quarter q = warp % 4, column quarter cq = warp / 4) owns row
+    // 32 q + lane and the columns [cq * NCQ, (cq + 1) * NCQ) of D1 | D2
+    const int NCQ = NCT / 4;  // NCT is a multiple of 16
     float acc[kAccPerThread];
 #pragma unroll
     for (int i = 0; i < kAccPerThread; ++i) acc[i] = 0.f;
-    const int q = warp & 3, hcol = (warp >> 2) * NCH;
+    const int q = warp & 3, qcol = (warp >> 2) * NCQ;
 
     auto drain = [&](int set) {
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(set * 256 + hcol);
-      constexpr int kBatch = 32;  // columns in flight per wait
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(set * 256 + qcol);
+      constexpr int kBatch = 28;  // columns in flight per wait
 #pragma unroll
       for (int b0 = 0; b0 < kAccPerThread; b0 += kBatch) {
         uint32_t v[kBatch];
 #pragma unroll
-        for (int j = 0; j < kBatch / 8; ++j) {
-          const int col = b0 + j * 8;
-          if (col < kAccPerThread && col < NCH)  // warp-uniform
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                         : "=r"(v[j * 8]), "=r"(v[j * 8 + 1]), "=r"(v[j * 8 + 2]), "=r"(v[j * 8 + 3]),
-                           "=r"(v[j * 8 + 4]), "=r"(v[j * 8 + 5]), "=r"(v[j * 8 + 6]), "=r"(v[j * 8 + 7])
+        for (int j = 0; j < kBatch / 4; ++j) {
+          const int col = b0 + j * 4;
+          if (col < NCQ)  // warp-uniform; static when TAPS is
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[j * 4]), "=r"(v[j * 4 + 1]), "=r"(v[j * 4 + 2]), "=r"(v[j * 4 + 3])
                          : "r"(taddr + col)
                          : "memory");
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < kBatch / 8; ++j) {
-          const int col = b0 + j * 8;
-          if (col < kAccPerThread && col < NCH) {
+        for (int j = 0; j < kBatch / 4; ++j) {
+          const int col = b0 + j * 4;
+          if (col < NCQ) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[col + i] += __uint_as_float(v[j * 8 + i]);
+            for (int i = 0; i < 4; ++i) acc[col + i] += __uint_as_float(v[j * 4 + i]);
           }
         }
       }
     };
+
+    // expand: warp w owns k chunk w % 8 (frames 4(w%8) .. +3) and every second row group; lane -> (row
+    // rg*8 + lane/4, frame + lane%4), so a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
+    const int kc = warp & 7, rg_first = warp >> 3;
+    const int k = kc * 4 + (lane & 3), r8 = lane >> 2;
+    const int word0 = kc * kCoreWords + lane;  // core (rg, kc) -> (rg * kKCores + kc) * 32 + lane
+    const int nrg_a = KMP / 8, nrg = NB / 8;
 
     issue_slab(0);
     for (int c = 0; c < nchunk; ++c) {
@@ -258,30 +273,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
         drain(b);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       }
-      // expand: warp w owns k chunk w (frames 4w .. 4w+3), lane -> (row rg*8 + lane/4, frame 4w + lane%4);
-      // a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
       const float* re = planes + (size_t)(2 * st) * plane_words;
       const float* im = re + plane_words;
       float* hi_buf = opbuf + (size_t)(2 * b) * buf_words;
       float* lo_buf = hi_buf + buf_words;
-      const int k = warp * 4 + (lane & 3), r8 = lane >> 2;
-      const float sq = sqrtf(wbuf[st * kKC + k]);
-      const int word0 = warp * kCoreWords + lane;  // core (rg, kc = warp) -> (rg * kKCores + warp) * 32 + lane
-      const int nrg_a = KMP / 8;
-      auto put = [&](int rg, float v) {
-        v *= sq;
-        const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-        hi_buf[rg * (kKCores * kCoreWords) + word0] = hi;
-        lo_buf[rg * (kKCores * kCoreWords) + word0] = v - hi;
-      };
-#pragma unroll 5
-      for (int rg = 0; rg < nrg_a; ++rg) {  // history window: element e = rg*8 + r8 of frame k is slab[k*M + e]
-        put(rg, re[k * M + rg * 8 + r8]);
-        put(nrg_a + rg, im[k * M + rg * 8 + r8]);
+      const float sq = sqrt_approx_tc(wbuf[st * kKC + k]);
+      const float* rk = re + k * M + r8;
+      const float* ik = im + k * M + r8;
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {  // up to 24 row groups (NB <= 192), two warps per k chunk
+        const int rg = rg_first + 2 * i;
+        if (rg < nrg) {
+          float v;
+          if (rg < nrg_a) v = rk[rg * 8];                              // Re a: element rg*8 + r8 of the window
+          else if (rg < 2 * nrg_a) v = ik[(rg - nrg_a) * 8];           // Im a
+          else if (rg == 2 * nrg_a) v = rk[H * M];                     // Re y (rows >= M are never read back)
+          else if (rg == 2 * nrg_a + 1) v = ik[H * M];                 // Im y
+          else v = 0.f;
+          v *= sq;
+          const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+          hi_buf[rg * (kKCores * kCoreWords) + word0] = hi;
+          lo_buf[rg * (kKCores * kCoreWords) + word0] = v - hi;
+        }
       }
-      put(2 * nrg_a, re[(k + H) * M + r8]);      // current frame (rows >= M of the block are never read back)
-      put(2 * nrg_a + 1, im[(k + H) * M + r8]);
-      for (int rg = 2 * nrg_a + 2; rg < NB / 8; ++rg) put(rg, 0.f);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core reads
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[b]);
@@ -293,22 +307,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
       drain(c & 1);
     }
     float* out = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT) +
-                 (long long)(q * 32 + lane) * NCT + hcol;
+                 (long long)(q * 32 + lane) * NCT + qcol;
 #pragma unroll
     for (int j = 0; j < kAccPerThread / 4; ++j)
-      if (j * 4 < NCH)
+      if (j * 4 < NCQ)
         reinterpret_cast<float4*>(out)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   __syncthreads();
-  if (warp == kTcWorkers / 32) {
+  if (warp == kTcWorkerWarps) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u) : "memory");
   }
 }
 
 // ---------------------------------------------------------------------------
-int wpe_tc_supported(int km, int M) { return tc_cols(km, M) <= 2 * kAccPerThread ? 1 : 0; }
+int wpe_tc_supported(int km, int M) { return tc_cols(km, M) <= 4 * kAccPerThread ? 1 : 0; }
 int wpe_tc_cell_floats(int km, int M) { return 128 * tc_cols(km, M); }
 int wpe_tc_rows(int km, int M) { return tc_rows(km, M); }
 
@@ -321,9 +335,15 @@ static cudaError_t launch_tc_m(const WpeArgs& a, int nseg, int F, cudaStream_t s
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
   // all 512 tensor-memory columns belong to one CTA: keep a second CTA off the SM
   smem = std::max<size_t>(smem, 120 * 1024);
-  cudaError_t e = cudaFuncSetAttribute(wpe_gram_tc_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  wpe_gram_tc_kernel<M><<<dim3(F, nseg), kTcThreads, smem, st>>>(a);
+  if (a.taps == 10) {
+    cudaError_t e = cudaFuncSetAttribute(wpe_gram_tc_kernel<M, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    wpe_gram_tc_kernel<M, 10><<<dim3(F, nseg), kTcThreads, smem, st>>>(a);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(wpe_gram_tc_kernel<M, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    wpe_gram_tc_kernel<M, 0><<<dim3(F, nseg), kTcThreads, smem, st>>>(a);
+  }
   return cudaGetLastError();
 }
 

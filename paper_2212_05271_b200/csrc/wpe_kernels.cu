@@ -264,8 +264,9 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
   const int ld = km + 1;
   cdbl* A = reinterpret_cast<cdbl*>(smem_f4);  // km x ld
   cdbl* B = A + (size_t)km * ld;               // km x M
+  double* diag0 = reinterpret_cast<double*>(B + (size_t)km * M);  // regularized diagonal, for the fallback
   __shared__ double s_tr;
-  __shared__ int s_fail;
+  __shared__ int s_fail, s_slot;
   const int tid = threadIdx.x, nth = blockDim.x;
   const float2* tiles = a.gram + (sd.wcell_off + (long long)f * sd.wchunks) * ntiles * kTileElems;
   const long long chunk_stride = (long long)ntiles * kTileElems;
@@ -339,7 +340,10 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
     s_tr = a.regularization * scale;
   }
   __syncthreads();
-  for (int i = tid; i < km; i += nth) A[i * ld + i].re += s_tr;
+  for (int i = tid; i < km; i += nth) {
+    A[i * ld + i].re += s_tr;
+    diag0[i] = A[i * ld + i].re;
+  }
   __syncthreads();
 
   // right-looking Cholesky on the lower triangle
@@ -362,9 +366,37 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
     __syncthreads();
   }
   if (s_fail) {
-    // TODO(eigen-floor fallback, numerics.hpp:58-73, 90-93): reported, not repaired
-    if (tid == 0) atomicMin(a.status + blockIdx.y, make_status(5, f));
+    // Eigenvalue-floor fallback (numerics.hpp:58-73, 90-93). Rare: one thread, FP64 cyclic Jacobi in a global
+    // scratch slot. The factorization only touched the lower triangle and the diagonal, so the regularized
+    // matrix is rebuilt from the untouched upper triangle and the saved diagonal; P is still intact.
     float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
+    if (tid == 0) {
+      const int t = atomicAdd(a.fb_ticket, 1);
+      s_slot = t < a.fb_slots ? t : -1;
+    }
+    __syncthreads();
+    if (s_slot >= 0) {
+      cdbl* Ag = a.fb_scratch + (size_t)s_slot * wpe_fallback_slot_elems(km, M);
+      cdbl* work = Ag + (size_t)km * km;
+      cdbl* work2 = work + (size_t)km * km;
+      cdbl* Bg = work2 + (size_t)km * km;
+      double* wv = reinterpret_cast<double*>(Bg + (size_t)km * M);
+      for (int idx = tid; idx < km * km; idx += nth) {
+        const int i = idx / km, j = idx - i * km;
+        Ag[idx] = i == j ? cd_make(diag0[i], 0.0) : (j > i ? A[i * ld + j] : cd_conj(A[j * ld + i]));
+      }
+      for (int idx = tid; idx < km * M; idx += nth) Bg[idx] = B[idx];
+      __threadfence_block();
+      __syncthreads();
+      if (tid == 0) s_fail = hermitian_solve(Ag, km, Bg, M, work, work2, wv) == kLinOk ? 2 : 3;
+      __threadfence_block();
+      __syncthreads();
+      if (s_fail == 2) {
+        for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2((float)Bg[idx].re, (float)(-Bg[idx].im));
+        return;
+      }
+    }
+    if (tid == 0) atomicMin(a.status + blockIdx.y, make_status(5, f));
     for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2(0.f, 0.f);
     return;
   }
@@ -463,6 +495,7 @@ __global__ void __launch_bounds__(256) wpe_apply_kernel(WpeArgs a) {
 // launchers
 // ---------------------------------------------------------------------------
 int wpe_gram_cell_elems(int km, int M) { return gram_num_tiles(km, M) * kTileElems; }
+int wpe_fallback_slot_elems_host(int km, int M) { return wpe_fallback_slot_elems(km, M); }
 
 template <int M>
 static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
@@ -482,7 +515,7 @@ static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F
     dim3 grid(ngroups * max_wchunks, F, nseg);
     wpe_gram_kernel<M><<<grid, kGramThreads, smem, st>>>(a);
   } else if (step == 2) {
-    const size_t smem = sizeof(cdbl) * ((size_t)km * (km + 1) + (size_t)km * M);
+    const size_t smem = sizeof(cdbl) * ((size_t)km * (km + 1) + (size_t)km * M) + sizeof(double) * km;
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(wpe_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

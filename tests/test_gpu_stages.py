@@ -137,6 +137,23 @@ def test_wpe_matches_oracle(gss, oracle, f, t, m, taps, delay, iters, ctx):
     assert again.tobytes() == got.tobytes()
 
 
+def test_wpe_eigen_floor_fallback(gss, oracle):
+    # numerics.hpp:58-73, 90-93 through the WPE solve: a silent channel and regularization 0 make R exactly
+    # singular, the Cholesky pivot is 0, and the solve must fall back to the eigenvalue floor like the oracle
+    rng = np.random.RandomState(12)
+    f, t, m, taps = 3, 400, 3, 4
+    s = (rng.randn(f, t, m) + 1j * rng.randn(f, t, m)).astype(np.complex64)
+    y = s.copy()
+    y[:, 2:, :] += 0.5 * s[:, :-2, :]
+    y[:, :, 1] = 0
+    cfg = gss.wpe.WpeConfig(taps, 2, 2, 0, 0.0)
+    got = gss.wpe.dereverberate(spec(gss, y), cfg).data
+    want = oracle.wpe(y, oracle.wpe_cfg(taps, 2, 2, 0, 0.0))
+    assert np.isfinite(got).all()
+    assert np.all(got[:, :, 1] == 0)
+    assert rel_fro(got, want) < 1e-4, rel_fro(got, want)
+
+
 # --------------------------------------------------------------------------- cACGMM
 def _em_problem(seed, f, t, m, k, noise=True):
     rng = np.random.RandomState(seed)
