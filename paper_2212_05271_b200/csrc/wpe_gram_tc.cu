@@ -27,9 +27,9 @@ namespace {
 constexpr int kTcWorkers = 512;             // 16 warps expand the operands and fold the accumulators
 constexpr int kTcWorkerWarps = kTcWorkers / 32;
 constexpr int kTcThreads = kTcWorkers + 32; // + one warp whose lane 0 issues the MMAs
-constexpr int kKC = 32;                     // frames per pipeline stage (4 MMA k-steps of 8); = 4 * kTcWarps
+constexpr int kKC = 64;                     // frames per pipeline stage (8 MMA k-steps of 8) = 4 per worker warp
 constexpr int kCoreWords = 32;              // one core matrix: 8 rows x 16 bytes
-constexpr int kKCores = kKC / 4;            // core matrices along K per row group (= kTcWarps)
+constexpr int kKCores = kKC / 4;            // core matrices along K per row group (= kTcWorkerWarps)
 constexpr int kLook = 8;                    // look-ahead frames read by the padded rows
 constexpr int kAccPerThread = 56;           // register accumulators per thread: NCT <= 224 columns / 4 quarters
 
@@ -224,36 +224,37 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
 
     auto drain = [&](int set) {
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(set * 256 + qcol);
-      constexpr int kBatch = 28;  // columns in flight per wait
+      constexpr int kBatch = 32;  // columns in flight per wait
 #pragma unroll
       for (int b0 = 0; b0 < kAccPerThread; b0 += kBatch) {
         uint32_t v[kBatch];
 #pragma unroll
-        for (int j = 0; j < kBatch / 4; ++j) {
-          const int col = b0 + j * 4;
-          if (col < NCQ)  // warp-uniform; static when TAPS is
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v[j * 4]), "=r"(v[j * 4 + 1]), "=r"(v[j * 4 + 2]), "=r"(v[j * 4 + 3])
+        for (int j = 0; j < kBatch / 8; ++j) {
+          const int col = b0 + j * 8;
+          if (col < kAccPerThread && col < NCQ)  // warp-uniform; static when TAPS is
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=r"(v[j * 8]), "=r"(v[j * 8 + 1]), "=r"(v[j * 8 + 2]), "=r"(v[j * 8 + 3]),
+                           "=r"(v[j * 8 + 4]), "=r"(v[j * 8 + 5]), "=r"(v[j * 8 + 6]), "=r"(v[j * 8 + 7])
                          : "r"(taddr + col)
                          : "memory");
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < kBatch / 4; ++j) {
-          const int col = b0 + j * 4;
-          if (col < NCQ) {
+        for (int j = 0; j < kBatch / 8; ++j) {
+          const int col = b0 + j * 8;
+          if (col < kAccPerThread && col < NCQ) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc[col + i] += __uint_as_float(v[j * 4 + i]);
+            for (int i = 0; i < 8; ++i) acc[col + i] += __uint_as_float(v[j * 8 + i]);
           }
         }
       }
     };
 
-    // expand: warp w owns k chunk w % 8 (frames 4(w%8) .. +3) and every second row group; lane -> (row
-    // rg*8 + lane/4, frame + lane%4), so a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
-    const int kc = warp & 7, rg_first = warp >> 3;
-    const int k = kc * 4 + (lane & 3), r8 = lane >> 2;
-    const int word0 = kc * kCoreWords + lane;  // core (rg, kc) -> (rg * kKCores + kc) * 32 + lane
+    // expand: warp w owns k chunk w (frames 4w .. 4w+3) and walks all row groups; lane -> (row rg*8 + lane/4,
+    // frame 4w + lane%4), so a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
+    static_assert(kTcWorkerWarps == kKCores, "one worker warp per K chunk");
+    const int k = warp * 4 + (lane & 3), r8 = lane >> 2;
+    const int word0 = warp * kCoreWords + lane;  // core (rg, kc = warp) -> (rg * kKCores + warp) * 32 + lane
     const int nrg_a = KMP / 8, nrg = NB / 8;
 
     issue_slab(0);
@@ -281,8 +282,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
       const float* rk = re + k * M + r8;
       const float* ik = im + k * M + r8;
 #pragma unroll
-      for (int i = 0; i < 12; ++i) {  // up to 24 row groups (NB <= 192), two warps per k chunk
-        const int rg = rg_first + 2 * i;
+      for (int rg = 0; rg < 24; ++rg) {  // NB <= 192 rows
         if (rg < nrg) {
           float v;
           if (rg < nrg_a) v = rk[rg * 8];                              // Re a: element rg*8 + r8 of the window
@@ -322,7 +322,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-int wpe_tc_supported(int km, int M) { return tc_cols(km, M) <= 4 * kAccPerThread ? 1 : 0; }
+int wpe_tc_supported(int km, int M) {
+  // accumulator columns per thread come in groups of 8 (tcgen05.ld x8) and must fit the register tile
+  return tc_cols(km, M) <= 4 * kAccPerThread && (tc_cols(km, M) / 4) % 8 == 0 ? 1 : 0;
+}
 int wpe_tc_cell_floats(int km, int M) { return 128 * tc_cols(km, M); }
 int wpe_tc_rows(int km, int M) { return tc_rows(km, M); }
 
@@ -332,7 +335,7 @@ static cudaError_t launch_tc_m(const WpeArgs& a, int nseg, int F, cudaStream_t s
   size_t off = 128 + sizeof(float) * (3 * kKC + 6 * (size_t)(kKC + H + kLook) * M);
   off = (off + 127) & ~(size_t)127;
   size_t smem = off + sizeof(float) * 4 * (size_t)tc_buf_rows(km, M) * kKC;
-  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+  if (smem > 224 * 1024) return cudaErrorInvalidConfiguration;
   // all 512 tensor-memory columns belong to one CTA: keep a second CTA off the SM
   smem = std::max<size_t>(smem, 120 * 1024);
   if (a.taps == 10) {
