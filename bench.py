@@ -31,11 +31,21 @@ UNIT = "audio-s/s"
 
 
 def _peaks():
+    """(HBM GB/s, dense bf16 TFLOP/s burst, source). TF32 tensor throughput is half the bf16 rate."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
-    return 6650.0, "fallback (B200_PROFILING.md)"
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def _ncu_traffic():
+    """DRAM bytes per launch and segment of each kernel class from the committed ncu --set full captures."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
 
 
 class ClockSampler(threading.Thread):
@@ -93,6 +103,12 @@ def algorithmic_work(segs, cfg):
             w["wpe_solve"]["flops"] += J * F * (8 / 3 * km ** 3 + 16 * km * km * M)
             w["wpe_apply"]["flops"] += J * FT * 8 * km * M
             w["wpe_apply"]["bytes"] += J * 2 * 8 * FT * M
+        if J:
+            # tensor-core Gram: executed TF32 flops (3xTF32 split, padded 128 x (NR + N2) real accumulator)
+            kmp = (km + 7) // 8 * 8
+            nr = (2 * kmp + 16 + 15) // 16 * 16
+            nct = nr + max(0, nr - 128)
+            w["wpe_gram"]["tensor_flops"] = w["wpe_gram"].get("tensor_flops", 0.0) + J * FT * 3 * 2 * 128 * nct
         w["em_pass"]["flops"] += (I + 1) * FT * (3 * M * M + 4 * M * M * K + 20 * K)
         w["em_pass"]["bytes"] += (I + 1) * (8 * FT * M + T * K)
         w["em_update"]["flops"] += (I + 1) * F * K * (8 * M ** 3)
@@ -168,9 +184,12 @@ def run_ours(args, rank, world, local_rank):
     value = out_s * args.steps / (ms_max * 1e-3)
     line = None
     if rank == 0:
-        hbm_peak, peak_src = _peaks()
+        hbm_peak, bf16_peak, peak_src = _peaks()
+        tf32_peak = 0.5 * bf16_peak
         fp32_peak = ctx.fp32_peak_tflops()
         work = algorithmic_work(wl.segments, cfg)
+        traffic = _ncu_traffic()
+        tc_gram = os.environ.get("GSS_B200_WPE_GRAM", "tc") != "fp32"
         kernels = {}
         for name, (kms_total, n) in kms.items():
             if n == 0 or name not in work:
@@ -185,14 +204,26 @@ def run_ours(args, rank, world, local_rank):
             kernels[name] = {"ms_per_step": round(per_step, 4), "launches_per_step": n // args.steps, "bound": bound,
                              "achieved": round(ach, 2), "peak": round(peak, 2),
                              "unit": "TFLOP/s" if bound == "fp32" else "GB/s", "frac": round(ach / peak, 4)}
+            if name == "wpe_gram" and tc_gram and "tensor_flops" in work[name]:
+                # tcgen05 kind::tf32: `achieved` stays the ALGORITHMIC (FP32-equivalent) rate; the executed tensor
+                # rate (3 MMAs per product, padded tiles) is reported beside it
+                ex = work[name]["tensor_flops"] / (per_step * 1e-3) * 1e-12
+                kernels[name].update({"bound": "tensor", "peak": round(tf32_peak, 2), "frac": round(ach / tf32_peak, 4),
+                                      "executed_tensor_tflops": round(ex, 1),
+                                      "executed_frac": round(ex / tf32_peak, 4),
+                                      "peak_note": "TF32 dense = 0.5 x bf16 " + peak_src})
+            if name in traffic:
+                kernels[name]["traffic_bytes_per_launch"] = int(traffic[name]["dram_bytes_per_segment_launch"] * nseg)
         top = max(kernels, key=lambda k: kernels[k]["ms_per_step"]) if kernels else None
         roof = None
         if top:
             k = kernels[top]
             roof = {"kernel": top, "bound": k["bound"], "achieved": k["achieved"], "peak": k["peak"], "unit": k["unit"],
-                    "frac": k["frac"], "traffic": None,
+                    "frac": k["frac"], "traffic": k.get("traffic_bytes_per_launch"),
+                    "algorithmic_per_launch": (work[top]["flops"] if k["bound"] != "hbm" else work[top]["bytes"])
+                    / max(1, k["launches_per_step"]),
                     "peak_source": ("measured FFMA loop in this run (gss_b200_fp32_peak)" if k["bound"] == "fp32"
-                                    else peak_src),
+                                    else k.get("peak_note", peak_src)),
                     "avg_launch_ms": round(k["ms_per_step"] / max(1, k["launches_per_step"]), 4),
                     "share_of_step": round(k["ms_per_step"] / (ms_max / args.steps), 4)}
         I = cfg.bss_iterations

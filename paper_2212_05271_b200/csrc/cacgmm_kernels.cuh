@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
   float* s_coef = reinterpret_cast<float*>(slab + 2 * TILE * FS);    // COEF_FLOATS (16-byte aligned)
   float* s_ck = s_coef + Cfg::COEF_FLOATS;                           // npat_max * KT
   unsigned char* s_pat = reinterpret_cast<unsigned char*>(s_ck + a.npat_max * KT);  // 2 * TILE
+  unsigned char* s_amask = s_pat + 2 * TILE;                                        // npat_max: active classes
 
   const int tid = threadIdx.x;
   const WorkItem wi = a.work[blockIdx.x];
@@ -213,6 +214,13 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
     const float* cks = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
     for (int i = tid; i < sd.npat * KT; i += kEmThreads) s_ck[i] = cks[i];
     for (int i = tid; i < min(TILE, nt); i += kEmThreads) s_pat[i] = psrc[i];
+    // classes that can be active under a pattern (finite constant); the others have gamma == 0 exactly
+    for (int p = tid; p < sd.npat; p += kEmThreads) {
+      unsigned m = 0;
+      for (int k = 0; k < KT; ++k)
+        if (cks[p * KT + k] != -CUDART_INF_F) m |= 1u << k;
+      s_amask[p] = (unsigned char)m;
+    }
   }
 
   const int lane = tid & 31, warp = tid >> 5;
@@ -276,25 +284,32 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
         const float inv = rcp_approx(nr);
         inv2 = inv * inv;
       }
+      // Classes that are inactive for every frame this warp holds are skipped (warp-uniform branches):
+      // speakers talk in long runs, so a warp's frames usually share one activity pattern.
+      const int pid = (int)sp[fbc];
+      const unsigned am = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid]);
       float q[KT];
 #pragma unroll
-      for (int k = 0; k < KT; ++k) q[k] = 0.f;
+      for (int k = 0; k < KT; ++k) {
+        if (am & (1u << k)) {
+          float s = 0.f;
 #pragma unroll
-      for (int j4 = 0; j4 < NDOFP / 4; ++j4)
+          for (int j4 = 0; j4 < NDOFP / 4; ++j4) {
+            const float4 c = c4[k * (NDOFP / 4) + j4];
+            s = fmaf(c.x, pv[4 * j4], s);
+            if (4 * j4 + 1 < NDOF) s = fmaf(c.y, pv[4 * j4 + 1 < NDOF ? 4 * j4 + 1 : 0], s);
+            if (4 * j4 + 2 < NDOF) s = fmaf(c.z, pv[4 * j4 + 2 < NDOF ? 4 * j4 + 2 : 0], s);
+            if (4 * j4 + 3 < NDOF) s = fmaf(c.w, pv[4 * j4 + 3 < NDOF ? 4 * j4 + 3 : 0], s);
+          }
 #pragma unroll
-        for (int k = 0; k < KT; ++k) {
-          const float4 c = c4[k * (NDOFP / 4) + j4];
-          q[k] = fmaf(c.x, pv[4 * j4], q[k]);
-          if (4 * j4 + 1 < NDOF) q[k] = fmaf(c.y, pv[4 * j4 + 1 < NDOF ? 4 * j4 + 1 : 0], q[k]);
-          if (4 * j4 + 2 < NDOF) q[k] = fmaf(c.z, pv[4 * j4 + 2 < NDOF ? 4 * j4 + 2 : 0], q[k]);
-          if (4 * j4 + 3 < NDOF) q[k] = fmaf(c.w, pv[4 * j4 + 3 < NDOF ? 4 * j4 + 3 : 0], q[k]);
+          for (int o = LM::G_LO; o < LM::G_HI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          q[k] = s;
+        } else {
+          q[k] = 1.f;  // its constant is -inf: the posterior is exactly 0 whatever q is
         }
-#pragma unroll
-      for (int o = LM::G_LO; o < LM::G_HI; o <<= 1)
-#pragma unroll
-        for (int k = 0; k < KT; ++k) q[k] += __shfl_xor_sync(0xffffffffu, q[k], o);
+      }
 
-      const float* ckp = s_ck + (int)sp[fbc] * KT;
+      const float* ckp = s_ck + pid * KT;
       float u[KT];
       float mx = -CUDART_INF_F;
 #pragma unroll
@@ -338,9 +353,11 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
       } else {
 #pragma unroll
         for (int k = 0; k < NA; ++k) {
-          const float w = u[k] * rinv2 * rcp_approx(q[k]);  // gamma / q on the unit-norm frame
+          if (am & (1u << k)) {
+            const float w = u[k] * rinv2 * rcp_approx(q[k]);  // gamma / q on the unit-norm frame
 #pragma unroll
-          for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w, pv[j], acc[k][j]);
+            for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w, pv[j], acc[k][j]);
+          }
         }
       }
     }
