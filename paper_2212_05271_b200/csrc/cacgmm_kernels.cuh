@@ -34,7 +34,9 @@ template <int M, int L>
 struct LaneMap {
   static constexpr bool SPREAD = L <= 4;
   static constexpr int SPW = 32 / L;  // frame slots per warp
-  static constexpr int STRIDE = !SPREAD ? M : (M == 7 ? 10 : M == 8 ? 10 : M == 4 ? 5 : M == 2 ? 3 : M);
+  static constexpr int STRIDE = !SPREAD ? M
+                                : L == 4 ? (M == 7 ? 10 : M == 8 ? 10 : M)
+                                         : (M == 8 ? 9 : M == 6 ? 7 : M == 4 ? 5 : M == 2 ? 3 : M);
   __device__ static __forceinline__ int g_of(int lane) { return SPREAD ? lane / SPW : lane % L; }
   __device__ static __forceinline__ int slot_of(int lane) { return SPREAD ? lane % SPW : lane / L; }
   /// xor offsets that stay inside a frame's lane group / that walk over the slots of a warp
@@ -278,12 +280,15 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
       const int fbc = valid ? fb : nin - 1;
       float pv[NDOF];
       plan.dofs(sl + fbc * FS, pv);
-      float inv2 = 1.f;
+      // Unit normalisation y/(|y|+1e-10) (wpe.hpp:135) scales every class's quadratic form by the same
+      // s^2 = 1/nr2, which cancels in the posteriors and in gamma/q * s^2; only the floor and the likelihood
+      // see it: max(q_raw s^2, 1e-10) = s^2 max(q_raw, 1e-10 nr2).
+      float nr2 = 1.f;
       if (normalize) {
-        const float nr = sqrt_approx(plan.norm2(pv)) + 1e-10f;  // wpe.hpp:135
-        const float inv = rcp_approx(nr);
-        inv2 = inv * inv;
+        const float nr = sqrt_approx(plan.norm2(pv)) + 1e-10f;
+        nr2 = nr * nr;
       }
+      const float qfloor = kQuadFloor * nr2;
       // Classes that are inactive for every frame this warp holds are skipped (warp-uniform branches):
       // speakers talk in long runs, so a warp's frames usually share one activity pattern.
       const int pid = (int)sp[fbc];
@@ -292,15 +297,16 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
         if (am & (1u << k)) {
-          float s = 0.f;
+          float s0 = 0.f, s1 = 0.f;  // two chains: half the dependent-FMA depth
 #pragma unroll
           for (int j4 = 0; j4 < NDOFP / 4; ++j4) {
             const float4 c = c4[k * (NDOFP / 4) + j4];
-            s = fmaf(c.x, pv[4 * j4], s);
-            if (4 * j4 + 1 < NDOF) s = fmaf(c.y, pv[4 * j4 + 1 < NDOF ? 4 * j4 + 1 : 0], s);
-            if (4 * j4 + 2 < NDOF) s = fmaf(c.z, pv[4 * j4 + 2 < NDOF ? 4 * j4 + 2 : 0], s);
-            if (4 * j4 + 3 < NDOF) s = fmaf(c.w, pv[4 * j4 + 3 < NDOF ? 4 * j4 + 3 : 0], s);
+            s0 = fmaf(c.x, pv[4 * j4], s0);
+            if (4 * j4 + 1 < NDOF) s1 = fmaf(c.y, pv[4 * j4 + 1 < NDOF ? 4 * j4 + 1 : 0], s1);
+            if (4 * j4 + 2 < NDOF) s0 = fmaf(c.z, pv[4 * j4 + 2 < NDOF ? 4 * j4 + 2 : 0], s0);
+            if (4 * j4 + 3 < NDOF) s1 = fmaf(c.w, pv[4 * j4 + 3 < NDOF ? 4 * j4 + 3 : 0], s1);
           }
+          float s = s0 + s1;
 #pragma unroll
           for (int o = LM::G_LO; o < LM::G_HI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
           q[k] = s;
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
       float mx = -CUDART_INF_F;
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
-        q[k] = fmaxf(q[k] * inv2, kQuadFloor);               // cacgmm.hpp:170-171
+        q[k] = fmaxf(q[k], qfloor);                           // cacgmm.hpp:170-171, in raw units
         // log2 domain: the table holds ck * log2(e); inactive classes carry ck = -inf
         u[k] = fmaf(-(float)M, lg2_approx(q[k]), ckp[k]);
         mx = fmaxf(mx, u[k]);
@@ -326,8 +332,8 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
         se += u[k];
       }
       const float rinv = valid ? rcp_approx(se) : 0.f;
-      if (valid && g == 0) ll += (double)(mx + lg2_approx(se));  // log2 units, scaled once at the end
-      const float rinv2 = rinv * inv2;
+      // log2 units, scaled once at the end; the common s^2 factor comes back here: -M log2(s^2) = +M log2(nr2)
+      if (valid && g == 0) ll += (double)(mx + lg2_approx(se) + (float)M * lg2_approx(nr2));
       float gam[KT];
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
 #pragma unroll
         for (int k = 0; k < NA; ++k) {
           if (am & (1u << k)) {
-            const float w = u[k] * rinv2 * rcp_approx(q[k]);  // gamma / q on the unit-norm frame
+            const float w = u[k] * rinv * rcp_approx(q[k]);  // (gamma / q s^2) on the raw frame
 #pragma unroll
             for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w, pv[j], acc[k][j]);
           }

@@ -346,22 +346,68 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
   }
   __syncthreads();
 
-  // right-looking Cholesky on the lower triangle
-  for (int k = 0; k < km; ++k) {
-    if (tid == 0) {
-      const double d = A[k * ld + k].re;
-      if (!(d > 0.0)) s_fail = 1;
-      A[k * ld + k] = cd_make(sqrt(d > 0.0 ? d : 1.0), 0.0);
+  // Blocked right-looking Cholesky on the lower triangle (panels of PB columns: 3 barriers per panel
+  // instead of 3 per column). A pivot <= 0 fails, Eigen LLT's criterion (numerics.hpp:88).
+  constexpr int PB = 8;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int kb = 0; kb < km; kb += PB) {
+    const int pb = min(PB, km - kb);
+    if (warp == 0) {  // 1. factor the diagonal block in place
+      cdbl* D = A + kb * ld + kb;
+      bool ok = true;
+      for (int k = 0; k < pb; ++k) {
+        const double d = D[k * ld + k].re;
+        if (!(d > 0.0)) {
+          ok = false;
+          break;  // warp-uniform
+        }
+        const double sq = sqrt(d), inv = 1.0 / sq;
+        __syncwarp();
+        if (lane == 0) D[k * ld + k] = cd_make(sq, 0.0);
+        if (lane > k && lane < pb) D[lane * ld + k] = cd_scale(D[lane * ld + k], inv);
+        __syncwarp();
+        const int r = pb - 1 - k;
+        if (lane < r * (r + 1) / 2) {
+          int ii = 0;
+          while ((ii + 1) * (ii + 2) / 2 <= lane) ++ii;
+          const int i = k + 1 + ii, jj = k + 1 + (lane - ii * (ii + 1) / 2);
+          D[i * ld + jj] = cd_sub(D[i * ld + jj], cd_mulc(D[i * ld + k], D[jj * ld + k]));
+        }
+        __syncwarp();
+      }
+      if (!ok && lane == 0) s_fail = 1;
     }
     __syncthreads();
     if (s_fail) break;
-    const double inv = 1.0 / A[k * ld + k].re;
-    for (int i = k + 1 + tid; i < km; i += nth) A[i * ld + k] = cd_scale(A[i * ld + k], inv);
+    const int r0 = kb + pb;  // first row below the panel
+    // 2. panel: row i of L21 solves x L11^H = A[i][kb..kb+pb)
+    for (int i = r0 + tid; i < km; i += nth) {
+      cdbl x[PB];
+#pragma unroll
+      for (int c = 0; c < PB; ++c) {
+        if (c < pb) {
+          cdbl sacc = A[i * ld + kb + c];
+#pragma unroll
+          for (int q = 0; q < PB; ++q)
+            if (q < c) sacc = cd_sub(sacc, cd_mulc(x[q], A[(kb + c) * ld + kb + q]));
+          x[c] = cd_scale(sacc, 1.0 / A[(kb + c) * ld + kb + c].re);
+          A[i * ld + kb + c] = x[c];
+        }
+      }
+    }
     __syncthreads();
-    for (int i = k + 1 + (tid >> 4); i < km; i += 16) {
-      const cdbl lik = A[i * ld + k];
-      for (int j = k + 1 + (tid & 15); j <= i; j += 16)
-        A[i * ld + j] = cd_sub(A[i * ld + j], cd_mulc(lik, A[j * ld + k]));
+    // 3. trailing update: A22 -= L21 L21^H (lower triangle)
+    for (int i = r0 + (tid >> 4); i < km; i += 16) {
+      cdbl li[PB];
+#pragma unroll
+      for (int c = 0; c < PB; ++c) li[c] = c < pb ? A[i * ld + kb + c] : cd_make(0.0, 0.0);
+      for (int jj = r0 + (tid & 15); jj <= i; jj += 16) {
+        cdbl sacc = A[i * ld + jj];
+#pragma unroll
+        for (int c = 0; c < PB; ++c)
+          if (c < pb) sacc = cd_sub(sacc, cd_mulc(li[c], A[jj * ld + kb + c]));
+        A[i * ld + jj] = sacc;
+      }
     }
     __syncthreads();
   }
@@ -400,24 +446,42 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
     for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2(0.f, 0.f);
     return;
   }
-  // forward: L Z = B
-  for (int k = 0; k < km; ++k) {
-    if (tid < M) B[k * M + tid] = cd_scale(B[k * M + tid], 1.0 / A[k * ld + k].re);
+  // forward: L Z = B, blocked like the factorization (thread c < M owns right-hand side c inside a panel)
+  for (int kb = 0; kb < km; kb += PB) {
+    const int pb = min(PB, km - kb);
+    if (tid < M) {
+      for (int k = 0; k < pb; ++k) {
+        cdbl sacc = B[(kb + k) * M + tid];
+        for (int q = 0; q < k; ++q) sacc = cd_sub(sacc, cd_mul(A[(kb + k) * ld + kb + q], B[(kb + q) * M + tid]));
+        B[(kb + k) * M + tid] = cd_scale(sacc, 1.0 / A[(kb + k) * ld + kb + k].re);
+      }
+    }
     __syncthreads();
-    const int rem = km - k - 1;
-    for (int idx = tid; idx < rem * M; idx += nth) {
-      const int i = k + 1 + idx / M, c = idx % M;
-      B[i * M + c] = cd_sub(B[i * M + c], cd_mul(A[i * ld + k], B[k * M + c]));
+    const int r0 = kb + pb;
+    for (int idx = tid; idx < (km - r0) * M; idx += nth) {
+      const int i = r0 + idx / M, c = idx % M;
+      cdbl sacc = B[i * M + c];
+      for (int q = 0; q < pb; ++q) sacc = cd_sub(sacc, cd_mul(A[i * ld + kb + q], B[(kb + q) * M + c]));
+      B[i * M + c] = sacc;
     }
     __syncthreads();
   }
   // backward: L^H X = Z
-  for (int k = km - 1; k >= 0; --k) {
-    if (tid < M) B[k * M + tid] = cd_scale(B[k * M + tid], 1.0 / A[k * ld + k].re);
+  for (int kb = ((km - 1) / PB) * PB; kb >= 0; kb -= PB) {
+    const int pb = min(PB, km - kb);
+    if (tid < M) {
+      for (int k = pb - 1; k >= 0; --k) {
+        cdbl sacc = B[(kb + k) * M + tid];
+        for (int q = k + 1; q < pb; ++q) sacc = cd_sub(sacc, cd_cmul(A[(kb + q) * ld + kb + k], B[(kb + q) * M + tid]));
+        B[(kb + k) * M + tid] = cd_scale(sacc, 1.0 / A[(kb + k) * ld + kb + k].re);
+      }
+    }
     __syncthreads();
-    for (int idx = tid; idx < k * M; idx += nth) {
+    for (int idx = tid; idx < kb * M; idx += nth) {
       const int i = idx / M, c = idx % M;
-      B[i * M + c] = cd_sub(B[i * M + c], cd_cmul(A[k * ld + i], B[k * M + c]));
+      cdbl sacc = B[i * M + c];
+      for (int q = 0; q < pb; ++q) sacc = cd_sub(sacc, cd_cmul(A[(kb + q) * ld + i], B[(kb + q) * M + c]));
+      B[i * M + c] = sacc;
     }
     __syncthreads();
   }
