@@ -36,6 +36,9 @@ def _mtime(p):
     return os.path.getmtime(p) if os.path.exists(p) else 0.0
 
 
+EXTRA_FLAGS: list[str] = []  # tools/variant.py: -D switches of a kernel experiment
+
+
 def _compile(src):
     obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
     spath = os.path.join(CSRC, src)
@@ -43,11 +46,22 @@ def _compile(src):
     if _mtime(obj) >= newest:
         return obj, 0, ""
     if src.endswith(".cu"):
-        cmd = [NVCC] + ARCH + [f for f in NVCC_FLAGS if not f.startswith("--use_fast_math")] + ["-c", spath, "-o", obj]
+        cmd = [NVCC] + ARCH + [f for f in NVCC_FLAGS if not f.startswith("--use_fast_math")] + EXTRA_FLAGS + ["-c", spath, "-o", obj]
     else:
         cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-I/usr/local/cuda/include", "-c", spath, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     return obj, r.returncode, r.stdout + r.stderr
+
+
+def build_variant(tag: str, flags: list[str], jobs: int | None = None) -> str:
+    """Same sources, extra -D flags, separate object dir and library name (lib/libgss_b200_<tag>.so)."""
+    global OBJ, LIB, EXTRA_FLAGS
+    saved = (OBJ, LIB, EXTRA_FLAGS)
+    try:
+        OBJ, LIB, EXTRA_FLAGS = os.path.join(HERE, "build", "variant_" + tag), os.path.join(LIB_DIR, f"libgss_b200_{tag}.so"), list(flags)
+        return build(False, jobs)
+    finally:
+        OBJ, LIB, EXTRA_FLAGS = saved
 
 
 def build(force: bool = False, jobs: int | None = None, verbose: bool = True) -> str:
@@ -55,7 +69,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = True) ->
     os.makedirs(LIB_DIR, exist_ok=True)
     if force:
         for f in os.listdir(OBJ):
-            os.remove(os.path.join(OBJ, f))
+            if os.path.isfile(os.path.join(OBJ, f)):
+                os.remove(os.path.join(OBJ, f))
     jobs = jobs or min(8, os.cpu_count() or 1)
     srcs = CU_SOURCES + CPP_SOURCES
     objs = []

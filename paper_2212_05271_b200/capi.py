@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libgss_b200.so")
+# GSS_B200_LIB points at another build of the SAME library (kernel experiments: tools/variant.py)
+LIB_PATH = os.environ.get("GSS_B200_LIB") or os.path.join(_HERE, "lib", "libgss_b200.so")
 
 NUM_STAGES = 7
 NUM_KERNELS = 11

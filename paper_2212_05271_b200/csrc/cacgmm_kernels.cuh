@@ -115,7 +115,7 @@ struct PartLayout {
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
-  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 __device__ __forceinline__ float lg2_approx(float x) {  // x >= 1e-10 here: no denormal inputs
@@ -130,7 +130,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
@@ -273,26 +273,27 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
     const int nin = min(TILE, nt - tile * TILE);
     const float2* sl = slab + buf * TILE * FS;
     const unsigned char* sp = s_pat + buf * TILE;
+    // The activity pattern of an iteration's frames (and the classes it can activate) is fetched one
+    // iteration ahead: the LDS -> LDS -> REDUX chain is off the critical path.
+    int pid_n = (int)sp[min(slot, nin - 1)];
+    unsigned am_n = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid_n]);
+    float llf = 0.f;  // this tile's log-likelihood terms (<= TILE / SLOTS of them) in float, folded into ll per tile
 #pragma unroll 1
     for (int fb = slot; fb < TILE; fb += SLOTS) {
       if (fb - slot >= nin) break;  // whole stripe of slots is past the data (block-uniform per warp row)
       const bool valid = fb < nin;
       const int fbc = valid ? fb : nin - 1;
+      const int pid = pid_n;
+      const unsigned am = am_n;
+      {
+        const int fbn = min(fb + SLOTS, nin - 1);
+        pid_n = (int)sp[fbn];
+        am_n = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid_n]);
+      }
       float pv[NDOF];
       plan.dofs(sl + fbc * FS, pv);
-      // Unit normalisation y/(|y|+1e-10) (wpe.hpp:135) scales every class's quadratic form by the same
-      // s^2 = 1/nr2, which cancels in the posteriors and in gamma/q * s^2; only the floor and the likelihood
-      // see it: max(q_raw s^2, 1e-10) = s^2 max(q_raw, 1e-10 nr2).
-      float nr2 = 1.f;
-      if (normalize) {
-        const float nr = sqrt_approx(plan.norm2(pv)) + 1e-10f;
-        nr2 = nr * nr;
-      }
-      const float qfloor = kQuadFloor * nr2;
       // Classes that are inactive for every frame this warp holds are skipped (warp-uniform branches):
       // speakers talk in long runs, so a warp's frames usually share one activity pattern.
-      const int pid = (int)sp[fbc];
-      const unsigned am = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid]);
       float q[KT];
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
@@ -306,14 +307,33 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
             if (4 * j4 + 2 < NDOF) s0 = fmaf(c.z, pv[4 * j4 + 2 < NDOF ? 4 * j4 + 2 : 0], s0);
             if (4 * j4 + 3 < NDOF) s1 = fmaf(c.w, pv[4 * j4 + 3 < NDOF ? 4 * j4 + 3 : 0], s1);
           }
-          float s = s0 + s1;
-#pragma unroll
-          for (int o = LM::G_LO; o < LM::G_HI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          q[k] = s;
+          q[k] = s0 + s1;
         } else {
-          q[k] = 1.f;  // its constant is -inf: the posterior is exactly 0 whatever q is
+          q[k] = 0.f;  // its constant is -inf: the posterior is exactly 0 whatever q is (floored below)
         }
       }
+      // One joint butterfly over the frame's L lanes for |y|^2 and every class's partial quadratic form:
+      // the KT + 1 shuffles of a stage are independent, so their latencies overlap.
+      float n2 = 0.f;
+      if (normalize) {
+#pragma unroll
+        for (int i = 0; i < Lay::RPL; ++i) n2 = fmaf(plan.rowmask[i], pv[i * M], n2);
+      }
+#pragma unroll
+      for (int o = LM::G_LO; o < LM::G_HI; o <<= 1) {
+        if (normalize) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+#pragma unroll
+        for (int k = 0; k < KT; ++k) q[k] += __shfl_xor_sync(0xffffffffu, q[k], o);
+      }
+      // Unit normalisation y/(|y|+1e-10) (wpe.hpp:135) scales every class's quadratic form by the same
+      // s^2 = 1/nr2, which cancels in the posteriors and in gamma/q * s^2; only the floor and the likelihood
+      // see it: max(q_raw s^2, 1e-10) = s^2 max(q_raw, 1e-10 nr2).
+      float nr2 = 1.f;
+      if (normalize) {
+        const float nr = sqrt_approx(n2) + 1e-10f;
+        nr2 = nr * nr;
+      }
+      const float qfloor = kQuadFloor * nr2;
 
       const float* ckp = s_ck + pid * KT;
       float u[KT];
@@ -333,7 +353,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
       }
       const float rinv = valid ? rcp_approx(se) : 0.f;
       // log2 units, scaled once at the end; the common s^2 factor comes back here: -M log2(s^2) = +M log2(nr2)
-      if (valid && g == 0) ll += (double)(mx + lg2_approx(se) + (float)M * lg2_approx(nr2));
+      if (valid && g == 0) llf += mx + lg2_approx(se) + (float)M * lg2_approx(nr2);
       float gam[KT];
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
@@ -360,13 +380,14 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
 #pragma unroll
         for (int k = 0; k < NA; ++k) {
           if (am & (1u << k)) {
-            const float w = u[k] * rinv * rcp_approx(q[k]);  // (gamma / q s^2) on the raw frame
+            const float w = gam[k] * rcp_approx(q[k]);  // (gamma / q s^2) on the raw frame
 #pragma unroll
             for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w, pv[j], acc[k][j]);
           }
         }
       }
     }
+    ll += (double)llf;
     __syncthreads();  // everyone is done with buffer `buf` (and with s_pat[buf])
     if (more) {
 #pragma unroll

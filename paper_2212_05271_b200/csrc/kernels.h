@@ -123,6 +123,9 @@ struct StatsFinalArgs {
 /// Lanes cooperating on one frame, chosen so the per-thread register tiles
 /// (2 * KT * NDOF floats) stay in registers.
 constexpr int em_lanes(int M, int KT) {
+#ifdef GSS_EXP_EM_LANES
+  if (M >= 5) return GSS_EXP_EM_LANES;
+#endif
   if (M == 1) return 1;
   if (M <= 4) return 2;
   if (M == 5) return KT <= 5 ? 2 : 4;

@@ -3,6 +3,12 @@
 import csv, sys, collections
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
+# a report with several captured launches repeats the header: keep the section asked for (default the first)
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Address"]
+sec = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+end = starts[sec + 1] - 1 if sec + 1 < len(starts) else len(rows)
+print(rows[starts[sec] - 1][1] if starts[sec] > 0 else "")
+rows = rows[:2] + rows[starts[sec] + 1:end]
 ix = {h: i for i, h in enumerate(hdr)}
 ops = collections.Counter(); samples = collections.Counter(); total = 0
 stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
