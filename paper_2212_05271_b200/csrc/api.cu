@@ -263,7 +263,7 @@ struct Group {
 };
 
 int pick_chunks(gss_b200_ctx* c, int T, long long ctas_one_chunk) {
-  const int slots_mult = 64;
+  const int slots_mult = 256;  // 8 warps x 32-frame groups of the sweep (cacgmm_pass2.cuh)
   int nch = 1;
   if (c->em_chunk_frames > 0) {
     nch = (T + c->em_chunk_frames - 1) / c->em_chunk_frames;

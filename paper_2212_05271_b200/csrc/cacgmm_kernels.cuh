@@ -134,6 +134,23 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return r;
 }
 
+// Packed FP32 pairs (Blackwell FFMA2): one issue slot for two fused multiply-adds, each rounded exactly like
+// a scalar fma.rn, so results are bit-identical to the scalar form.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pack2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
@@ -234,15 +251,20 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
       s_coef[(gk / KT) * Cfg::COEF_G + (gk % KT) * NDOFP + j] = j < NDOF ? cp[gk * NDOF + j] : 0.f;
     }
   }
-  const float4* c4 = reinterpret_cast<const float4*>(s_coef + g * Cfg::COEF_G);
-  float acc[NA][NDOF];
+  const ulonglong2* c4 = reinterpret_cast<const ulonglong2*>(s_coef + g * Cfg::COEF_G);
+  constexpr int NP = NDOF / 2;            // packed pairs of dofs
+  constexpr bool ODD = (NDOF & 1) != 0;   // + one scalar dof
+  f32x2 acc2[NA][NP > 0 ? NP : 1];
+  float acc1[NA];
   float mass[KT];
 #pragma unroll
   for (int k = 0; k < KT; ++k) mass[k] = 0.f;
 #pragma unroll
-  for (int n = 0; n < NA; ++n)
+  for (int n = 0; n < NA; ++n) {
+    acc1[n] = 0.f;
 #pragma unroll
-    for (int j = 0; j < NDOF; ++j) acc[n][j] = 0.f;
+    for (int j = 0; j < NP; ++j) acc2[n][j] = 0ull;
+  }
   double ll = 0.0;
   FramePlan<M, L> plan;
   plan.init(g);
@@ -292,22 +314,32 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
       }
       float pv[NDOF];
       plan.dofs(sl + fbc * FS, pv);
+      f32x2 pv2[NP > 0 ? NP : 1];
+#pragma unroll
+      for (int j = 0; j < NP; ++j) pv2[j] = pack2(pv[2 * j], pv[2 * j + 1]);
       // Classes that are inactive for every frame this warp holds are skipped (warp-uniform branches):
       // speakers talk in long runs, so a warp's frames usually share one activity pattern.
       float q[KT];
 #pragma unroll
       for (int k = 0; k < KT; ++k) {
         if (am & (1u << k)) {
-          float s0 = 0.f, s1 = 0.f;  // two chains: half the dependent-FMA depth
+          // even dofs accumulate in the low half, odd dofs in the high half (two chains)
+          f32x2 s2 = 0ull;
+          float s1 = 0.f;
 #pragma unroll
           for (int j4 = 0; j4 < NDOFP / 4; ++j4) {
-            const float4 c = c4[k * (NDOFP / 4) + j4];
-            s0 = fmaf(c.x, pv[4 * j4], s0);
-            if (4 * j4 + 1 < NDOF) s1 = fmaf(c.y, pv[4 * j4 + 1 < NDOF ? 4 * j4 + 1 : 0], s1);
-            if (4 * j4 + 2 < NDOF) s0 = fmaf(c.z, pv[4 * j4 + 2 < NDOF ? 4 * j4 + 2 : 0], s0);
-            if (4 * j4 + 3 < NDOF) s1 = fmaf(c.w, pv[4 * j4 + 3 < NDOF ? 4 * j4 + 3 : 0], s1);
+            const ulonglong2 c = c4[k * (NDOFP / 4) + j4];
+            if (2 * j4 < NP) s2 = ffma2(c.x, pv2[2 * j4 < NP ? 2 * j4 : 0], s2);
+            if (2 * j4 + 1 < NP) s2 = ffma2(c.y, pv2[2 * j4 + 1 < NP ? 2 * j4 + 1 : 0], s2);
+            if (ODD && (NDOF - 1) / 4 == j4) {  // the scalar tail dof sits in this quad
+              float c0, c1;
+              unpack2(((NDOF - 1) & 2) ? c.y : c.x, c0, c1);
+              s1 = c0 * pv[NDOF - 1];
+            }
           }
-          q[k] = s0 + s1;
+          float sa, sb;
+          unpack2(s2, sa, sb);
+          q[k] = NP > 0 ? (sa + sb) + s1 : s1;
         } else {
           q[k] = 0.f;  // its constant is -inf: the posterior is exactly 0 whatever q is (floored below)
         }
@@ -371,18 +403,25 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
           wt += (k == target) ? gam[k] : 0.f;
           wb += (k == target) ? 0.f : gam[k];
         }
+        const f32x2 wt2 = pack2(wt, wt), wb2 = pack2(wb, wb);
 #pragma unroll
-        for (int j = 0; j < NDOF; ++j) {
-          acc[0][j] = fmaf(wt, pv[j], acc[0][j]);
-          acc[NA - 1][j] = fmaf(wb, pv[j], acc[NA - 1][j]);
+        for (int j = 0; j < NP; ++j) {
+          acc2[0][j] = ffma2(wt2, pv2[j], acc2[0][j]);
+          acc2[NA - 1][j] = ffma2(wb2, pv2[j], acc2[NA - 1][j]);
+        }
+        if (ODD) {
+          acc1[0] = fmaf(wt, pv[NDOF - 1], acc1[0]);
+          acc1[NA - 1] = fmaf(wb, pv[NDOF - 1], acc1[NA - 1]);
         }
       } else {
 #pragma unroll
         for (int k = 0; k < NA; ++k) {
           if (am & (1u << k)) {
             const float w = gam[k] * rcp_approx(q[k]);  // (gamma / q s^2) on the raw frame
+            const f32x2 w2 = pack2(w, w);
 #pragma unroll
-            for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w, pv[j], acc[k][j]);
+            for (int j = 0; j < NP; ++j) acc2[k][j] = ffma2(w2, pv2[j], acc2[k][j]);
+            if (ODD) acc1[k] = fmaf(w, pv[NDOF - 1], acc1[k]);
           }
         }
       }
@@ -397,6 +436,13 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
 
   // ---- reduce: frame slots within the warp, then warps through shared memory
   ll = g != 0 ? 0.0 : ll * 0.69314718055994530942;  // back to natural-log units
+  float acc[NA][NDOF];
+#pragma unroll
+  for (int n = 0; n < NA; ++n) {
+#pragma unroll
+    for (int j = 0; j < NP; ++j) unpack2(acc2[n][j], acc[n][2 * j], acc[n][2 * j + 1]);
+    if (ODD) acc[n][NDOF - 1] = acc1[n];
+  }
 #pragma unroll
   for (int o = LM::S_LO; o < LM::S_HI; o <<= 1) {
 #pragma unroll

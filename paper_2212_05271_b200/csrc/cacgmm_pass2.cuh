@@ -1,0 +1,364 @@
+// cacgmm_pass2.cuh -- the cACGMM sweep (E-step + M-step / MVDR accumulation), second design.
+//
+// Reference semantics: cacgmm.hpp:156-174 (quad_forms), :189-257 (estep_bin), :308-329 (M-step Gram),
+// wpe.hpp:124-140 (unit_normalize, folded in), beamform.hpp:35-85 (accumulate_stats, last sweep).
+//
+// Why a second design. The first sweep (em_pass_kernel) gives every frame to L lanes and each of them
+// repeats the frame's soft-max, pattern lookup and loop control: at M = 7, K = 4 only 46 % of its issued
+// instructions were FP32 math (ncu, profiles/ncu_full_r01.md). Here a warp works on groups of 32 frames in
+// two phases with different lane maps:
+//
+//   phase A  lane = frame. The lane forms the M^2 Hermitian degrees of freedom ("dofs") of P = y y^H once,
+//            feeds each into the K quadratic forms (coefficients are warp-uniform shared-memory broadcasts),
+//            runs the guide-masked soft-max ONCE per frame without any shuffle, and parks the dofs (float4
+//            chunks, XOR-swizzled) and the K accumulation weights in the warp's shared-memory scratch.
+//   phase B  lane = (frame slot, dof slice g of L), the register layout of the accumulators (em_layout.cuh).
+//            Per frame a lane fetches its NDOF dofs as float4s and the weights, and does K * NDOF FMAs.
+//
+// No block-wide barrier in the main loop: frames are read straight from global memory one group ahead
+// (a warp's 32 frames are one contiguous run of 32 * M * 8 bytes), the scratch is private to the warp.
+// Output cells are identical in layout to em_pass_kernel's, so em_update_kernel is shared.
+#pragma once
+
+#include "cacgmm_kernels.cuh"
+
+namespace gssb {
+
+constexpr int pow2_ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+template <int M, int L, int KT, bool FINAL>
+struct EmPass2Cfg {
+  using Lay = EmLayout<M, L>;
+  static constexpr int NDOF = Lay::NDOF;
+  static constexpr int NDOFP = (NDOF + 3) & ~3;
+  static constexpr int CPG = NDOFP / 4;            // float4 chunks per lane slice g
+  static constexpr int NCH = L * CPG;              // chunks per frame
+  static constexpr int NCHP = pow2_ceil(NCH);      // frame stride of the dof scratch (float4 units)
+  static constexpr int KTP = KT <= 2 ? 2 : KT <= 4 ? 4 : 8;  // padded class count of the tables
+  static constexpr int NA = FINAL ? 2 : KT;
+  static constexpr int WS = FINAL ? 2 : KTP;       // weights parked per frame
+  static constexpr int SPW = 32 / L;               // frames per phase-B step
+  static constexpr int NW = kEmThreads / 32;
+  static constexpr int COEF_FLOATS = L * NDOFP * KTP;
+  static constexpr int WARP_SCRATCH_FLOATS = 32 * NCHP * 4 + 32 * WS;
+  // accumulators + two groups of frames in flight must fit the register file at this occupancy
+  static constexpr int MINB = (NA * NDOF + 4 * M <= 88) ? 2 : 1;
+};
+
+template <int M, int L, int KT, int MODE>
+__global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSweepFinal>::MINB)
+    em_pass2_kernel(EmPassArgs a) {
+  constexpr bool FINAL = MODE == kSweepFinal;
+  using Cfg = EmPass2Cfg<M, L, KT, FINAL>;
+  using Lay = EmLayout<M, L>;
+  constexpr int NDOF = Cfg::NDOF, NDOFP = Cfg::NDOFP, CPG = Cfg::CPG, NCHP = Cfg::NCHP, KTP = Cfg::KTP;
+  constexpr int NA = Cfg::NA, WS = Cfg::WS, SPW = Cfg::SPW, NW = Cfg::NW;
+  using PL = PartLayout<M, L, KT, NA>;
+  extern __shared__ float4 smem_f4[];
+  float* s_coef = reinterpret_cast<float*>(smem_f4);          // [g][idx][KTP]
+  float* s_ck = s_coef + Cfg::COEF_FLOATS;                    // [pattern][KTP]
+  const int ck_floats = (a.npat_max * KTP + 3) & ~3;
+  float* s_scratch = s_ck + ck_floats;                        // NW x WARP_SCRATCH_FLOATS (16-byte aligned)
+  unsigned char* s_amask = reinterpret_cast<unsigned char*>(s_scratch + NW * Cfg::WARP_SCRATCH_FLOATS);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const WorkItem wi = a.work[blockIdx.x];
+  const int f = blockIdx.y;
+  const SegDev sd = a.segs[wi.seg];
+  const int t0 = wi.chunk * sd.TC;
+  const int nt = min(sd.TC, sd.T - t0);
+  const int ngroups = (nt + 31) >> 5;
+  const float2* src = a.y + sd.y_off + ((long long)f * sd.T + t0) * M;
+  const unsigned char* psrc = a.pat + sd.pat_off + t0;
+
+  // ---- tables of this (segment, bin)
+  {
+    const float* cp = a.coef + sd.coef_off + (long long)f * L * (KT * NDOF);  // [g][k][j]
+    for (int i = tid; i < Cfg::COEF_FLOATS; i += kEmThreads) {
+      const int k = i % KTP, gj = i / KTP, j = gj % NDOFP, g = gj / NDOFP;
+      s_coef[i] = (k < KT && j < NDOF) ? cp[(g * KT + k) * NDOF + j] : 0.f;
+    }
+    const float* cks = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
+    for (int i = tid; i < sd.npat * KTP; i += kEmThreads) {
+      const int k = i % KTP, p = i / KTP;
+      s_ck[i] = k < KT ? cks[p * KT + k] : -CUDART_INF_F;
+    }
+    // classes that can be active under a pattern (finite constant); the others have gamma == 0 exactly
+    for (int p = tid; p < sd.npat; p += kEmThreads) {
+      unsigned m = 0;
+      for (int k = 0; k < KT; ++k)
+        if (cks[p * KT + k] != -CUDART_INF_F) m |= 1u << k;
+      s_amask[p] = (unsigned char)m;
+    }
+  }
+  __syncthreads();
+
+  float4* pbuf = reinterpret_cast<float4*>(s_scratch + warp * Cfg::WARP_SCRATCH_FLOATS);  // [32][NCHP]
+  float* wbuf = reinterpret_cast<float*>(pbuf + 32 * NCHP);                               // [32][WS]
+  const int g = lane / SPW, slot = lane % SPW;  // phase-B role
+
+  float acc[NA][NDOF];
+  float mass[KT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) mass[k] = 0.f;
+#pragma unroll
+  for (int n = 0; n < NA; ++n)
+#pragma unroll
+    for (int j = 0; j < NDOF; ++j) acc[n][j] = 0.f;
+  double ll = 0.0;
+  float* gout = MODE != kSweepEM && a.gamma != nullptr && sd.g_off >= 0
+                    ? a.gamma + sd.g_off + ((long long)f * sd.T + t0) * sd.K
+                    : nullptr;
+  const int target = sd.target;
+  const bool normalize = a.normalize != 0;
+
+  // frames of the first group (lane = frame; lanes past the end re-read the last frame and are masked)
+  float2 y[M];
+  int pid = 0;
+  if (warp < ngroups) {
+    const int tc = min(warp * 32 + lane, nt - 1);
+#pragma unroll
+    for (int m = 0; m < M; ++m) y[m] = src[(long long)tc * M + m];
+    pid = (int)psrc[tc];
+  }
+
+#pragma unroll 1
+  for (int grp = warp; grp < ngroups; grp += NW) {
+    const int t = grp * 32 + lane;
+    const bool valid = t < nt;
+    // prefetch the next group of this warp; it is consumed one iteration later
+    float2 yn[M];
+    int pidn = 0;
+    {
+      const int gn = grp + NW;
+      const int tc = min(gn * 32 + lane, nt - 1);
+      if (gn < ngroups) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) yn[m] = src[(long long)tc * M + m];
+        pidn = (int)psrc[tc];
+      } else {
+#pragma unroll
+        for (int m = 0; m < M; ++m) yn[m] = make_float2(0.f, 0.f);
+      }
+    }
+
+    // ================= phase A: lane = frame =================
+    float q[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) q[k] = 0.f;
+    float n2 = 0.f;
+#pragma unroll
+    for (int gg = 0; gg < L; ++gg) {
+      float pg[NDOFP];
+#pragma unroll
+      for (int j = 0; j < NDOFP; ++j) pg[j] = 0.f;
+#pragma unroll
+      for (int i = 0; i < Lay::RPL; ++i) {
+        const int row = gg + i * L;
+        if (row < M) {
+          const float2 x = y[row];
+#pragma unroll
+          for (int jr = 0; jr < M; ++jr) {
+            float p;
+            if (jr == 0) {
+              p = fmaf(x.x, x.x, x.y * x.y);
+              n2 += p;
+            } else if (jr <= 2 * Lay::D) {
+              const float2 z = y[(row + (jr + 1) / 2) % M];
+              p = (jr & 1) ? fmaf(x.x, z.x, x.y * z.y) : fmaf(x.y, z.x, -(x.x * z.y));
+            } else {  // half diagonal (M even)
+              const float2 z = y[(row + M / 2) % M];
+              p = row < M / 2 ? fmaf(x.x, z.x, x.y * z.y) : fmaf(x.y, z.x, -(x.x * z.y));
+            }
+            pg[i * M + jr] = p;
+            const float* c = s_coef + (gg * NDOFP + i * M + jr) * KTP;  // warp-uniform address: broadcast
+            if (KTP == 2) {
+              const float2 c2 = *reinterpret_cast<const float2*>(c);
+              q[0] = fmaf(c2.x, p, q[0]);
+              if (KT > 1) q[KT > 1 ? 1 : 0] = fmaf(c2.y, p, q[KT > 1 ? 1 : 0]);
+            } else {
+#pragma unroll
+              for (int k4 = 0; k4 < KTP / 4; ++k4) {
+                const float4 c4 = reinterpret_cast<const float4*>(c)[k4];
+                if (4 * k4 + 0 < KT) q[4 * k4 + 0 < KT ? 4 * k4 + 0 : 0] = fmaf(c4.x, p, q[4 * k4 + 0 < KT ? 4 * k4 + 0 : 0]);
+                if (4 * k4 + 1 < KT) q[4 * k4 + 1 < KT ? 4 * k4 + 1 : 0] = fmaf(c4.y, p, q[4 * k4 + 1 < KT ? 4 * k4 + 1 : 0]);
+                if (4 * k4 + 2 < KT) q[4 * k4 + 2 < KT ? 4 * k4 + 2 : 0] = fmaf(c4.z, p, q[4 * k4 + 2 < KT ? 4 * k4 + 2 : 0]);
+                if (4 * k4 + 3 < KT) q[4 * k4 + 3 < KT ? 4 * k4 + 3 : 0] = fmaf(c4.w, p, q[4 * k4 + 3 < KT ? 4 * k4 + 3 : 0]);
+              }
+            }
+          }
+        }
+      }
+      // park this slice's dofs: chunk (gg, c) of frame `lane` at swizzled position (conflict-free both ways)
+#pragma unroll
+      for (int c = 0; c < CPG; ++c)
+        pbuf[lane * NCHP + ((gg * CPG + c) ^ (lane & (NCHP - 1)))] =
+            make_float4(pg[4 * c], pg[4 * c + 1], pg[4 * c + 2], pg[4 * c + 3]);
+    }
+
+    // Unit normalisation y/(|y|+1e-10) (wpe.hpp:135) scales every class's quadratic form by the same
+    // s^2 = 1/nr2, which cancels in the posteriors and in gamma/q * s^2; only the floor and the likelihood
+    // see it: max(q_raw s^2, 1e-10) = s^2 max(q_raw, 1e-10 nr2).
+    float nr2 = 1.f;
+    if (normalize) {
+      const float nr = sqrt_approx(n2) + 1e-10f;
+      nr2 = nr * nr;
+    }
+    const float qfloor = kQuadFloor * nr2;
+    const float* ckp = s_ck + pid * KTP;
+    const unsigned am = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid]);
+    float u[KT];
+    float mx = -CUDART_INF_F;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      q[k] = fmaxf(q[k], qfloor);                            // cacgmm.hpp:170-171, in raw units
+      // log2 domain: the table holds ck * log2(e); inactive classes carry ck = -inf
+      u[k] = fmaf(-(float)M, lg2_approx(q[k]), ckp[k]);
+      mx = fmaxf(mx, u[k]);
+    }
+    float se = 0.f;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      u[k] = ex2_approx(u[k] - mx);
+      se += u[k];
+    }
+    const float rinv = valid ? rcp_approx(se) : 0.f;
+    // log2 units, scaled once at the end; the common s^2 factor comes back here: -M log2(s^2) = +M log2(nr2)
+    if (valid) ll += (double)(mx + lg2_approx(se) + (float)M * lg2_approx(nr2));
+    float gam[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      gam[k] = u[k] * rinv;  // exactly 0 for inactive classes and for lanes past the end
+      mass[k] += gam[k];
+    }
+    if (MODE != kSweepEM) {
+      if (gout != nullptr && valid) {
+        float* go = gout + (long long)t * sd.K;
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+          if (k < sd.K) go[k] = gam[k];
+      }
+    }
+    if (FINAL) {
+      float wt = 0.f, wb = 0.f;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        wt += (k == target) ? gam[k] : 0.f;
+        wb += (k == target) ? 0.f : gam[k];
+      }
+      *reinterpret_cast<float2*>(wbuf + lane * WS) = make_float2(wt, wb);
+    } else {
+      float w[KTP];
+#pragma unroll
+      for (int k = 0; k < KTP; ++k) w[k] = k < KT ? gam[k < KT ? k : 0] * rcp_approx(q[k < KT ? k : 0]) : 0.f;  // gamma / (q s^2)
+      if (KTP == 2) {
+        *reinterpret_cast<float2*>(wbuf + lane * WS) = make_float2(w[0], w[1]);
+      } else {
+#pragma unroll
+        for (int k4 = 0; k4 < KTP / 4; ++k4)
+          reinterpret_cast<float4*>(wbuf + lane * WS)[k4] = make_float4(w[4 * k4], w[4 * k4 + 1], w[4 * k4 + 2], w[4 * k4 + 3]);
+      }
+    }
+    __syncwarp();
+
+    // ================= phase B: lane = (frame slot, dof slice g) =================
+#pragma unroll
+    for (int step = 0; step < L; ++step) {
+      const int fr = step * SPW + slot;
+      float pv[NDOFP];
+#pragma unroll
+      for (int c = 0; c < CPG; ++c) {
+        const float4 v = pbuf[fr * NCHP + ((g * CPG + c) ^ (fr & (NCHP - 1)))];
+        pv[4 * c] = v.x;
+        pv[4 * c + 1] = v.y;
+        pv[4 * c + 2] = v.z;
+        pv[4 * c + 3] = v.w;
+      }
+      float w[WS];
+      if (WS == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(wbuf + fr * WS);
+        w[0] = v.x;
+        w[1] = v.y;
+      } else {
+#pragma unroll
+        for (int k4 = 0; k4 < WS / 4; ++k4) {
+          const float4 v = reinterpret_cast<const float4*>(wbuf + fr * WS)[k4];
+          w[4 * k4] = v.x;
+          w[4 * k4 + 1] = v.y;
+          w[4 * k4 + 2] = v.z;
+          w[4 * k4 + 3] = v.w;
+        }
+      }
+      if (FINAL) {
+#pragma unroll
+        for (int j = 0; j < NDOF; ++j) {
+          acc[0][j] = fmaf(w[0], pv[j], acc[0][j]);
+          acc[NA - 1][j] = fmaf(w[1], pv[j], acc[NA - 1][j]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+          if (am & (1u << k)) {  // warp-uniform: classes inactive for all 32 frames are skipped
+#pragma unroll
+            for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w[k], pv[j], acc[k][j]);
+          }
+        }
+      }
+    }
+    __syncwarp();  // the scratch is rewritten by the next group's phase A
+
+#pragma unroll
+    for (int m = 0; m < M; ++m) y[m] = yn[m];
+    pid = pidn;
+  }
+
+  // ---- reduce: frame slots within the warp, then warps through shared memory
+#pragma unroll
+  for (int o = 1; o < SPW; o <<= 1) {
+#pragma unroll
+    for (int n = 0; n < NA; ++n)
+#pragma unroll
+      for (int j = 0; j < NDOF; ++j) acc[n][j] += __shfl_xor_sync(0xffffffffu, acc[n][j], o);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int k = 0; k < KT; ++k) mass[k] += __shfl_xor_sync(0xffffffffu, mass[k], o);
+    ll += __shfl_xor_sync(0xffffffffu, ll, o);
+  }
+  ll *= 0.69314718055994530942;  // back to natural-log units
+  __syncthreads();               // every warp is done with its scratch
+  float* red = s_scratch;
+  double* redll = reinterpret_cast<double*>(red + NW * PL::CELL + (NW * PL::CELL & 1));
+  if (slot == 0) {
+    float* r = red + (warp * L + g) * PL::STRIDE;
+#pragma unroll
+    for (int n = 0; n < NA; ++n)
+#pragma unroll
+      for (int j = 0; j < NDOF; ++j) r[n * NDOF + j] = acc[n][j];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) r[PL::ACC + k] = mass[k];
+  }
+  if (lane == 0) redll[warp] = ll;
+  __syncthreads();
+  const long long cell = sd.cell_off + (long long)f * sd.nchunks + wi.chunk;
+  float* out = a.part + cell * a.cell_stride;
+  for (int i = tid; i < PL::CELL; i += kEmThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[w * PL::CELL + i];
+    out[i] = s;
+  }
+  if (tid == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += redll[w];
+    a.cell_ll[cell] = s;
+  }
+}
+
+}  // namespace gssb
