@@ -15,8 +15,8 @@
 //   phase B  lane = (frame slot, dof slice g of L), the register layout of the accumulators (em_layout.cuh).
 //            Per frame a lane fetches its NDOF dofs as float4s and the weights, and does K * NDOF FMAs.
 //
-// No block-wide barrier in the main loop: frames are read straight from global memory one group ahead
-// (a warp's 32 frames are one contiguous run of 32 * M * 8 bytes), the scratch is private to the warp.
+// No block-wide barrier in the main loop: each warp streams its own groups of frames (one contiguous run of
+// 32 * M * 8 bytes) through a private two-stage cp.async buffer, and the scratch is private to the warp.
 // Output cells are identical in layout to em_pass_kernel's, so em_update_kernel is shared.
 #pragma once
 
@@ -44,9 +44,17 @@ struct EmPass2Cfg {
   static constexpr int SPW = 32 / L;               // frames per phase-B step
   static constexpr int NW = kEmThreads / 32;
   static constexpr int COEF_FLOATS = L * NDOFP * KTP;
-  static constexpr int WARP_SCRATCH_FLOATS = 32 * NCHP * 4 + 32 * WS;
+  static constexpr int YSTAGE_FLOATS = 32 * M * 2;  // one group of frames (cp.async landing zone)
+  // per warp: dof scratch [32][NCHP] float4 | weights [32][WS] | two frame stages; a multiple of 256 bytes
+  static constexpr int WARP_SCRATCH_FLOATS = (32 * NCHP * 4 + 32 * WS + 2 * YSTAGE_FLOATS + 63) & ~63;
+  // epilogue dump: every thread parks its accumulators, stride chosen odd in float4 units (conflict-free)
+  static constexpr int DUMP_STRIDE = ((NA * NDOF + 3) / 4 | 1) * 4;
   // accumulators + two groups of frames in flight must fit the register file at this occupancy
+#ifdef GSS_EXP_MINB
+  static constexpr int MINB = GSS_EXP_MINB;
+#else
   static constexpr int MINB = (NA * NDOF + 4 * M <= 88) ? 2 : 1;
+#endif
 };
 
 template <int M, int L, int KT, int MODE>
@@ -57,12 +65,14 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   using Lay = EmLayout<M, L>;
   constexpr int NDOF = Cfg::NDOF, NDOFP = Cfg::NDOFP, CPG = Cfg::CPG, NCHP = Cfg::NCHP, KTP = Cfg::KTP;
   constexpr int NA = Cfg::NA, WS = Cfg::WS, SPW = Cfg::SPW, NW = Cfg::NW;
+  constexpr bool CPG_POW2 = (CPG & (CPG - 1)) == 0;
   using PL = PartLayout<M, L, KT, NA>;
   extern __shared__ float4 smem_f4[];
   float* s_coef = reinterpret_cast<float*>(smem_f4);          // [g][idx][KTP]
   float* s_ck = s_coef + Cfg::COEF_FLOATS;                    // [pattern][KTP]
   const int ck_floats = (a.npat_max * KTP + 3) & ~3;
-  float* s_scratch = s_ck + ck_floats;                        // NW x WARP_SCRATCH_FLOATS (16-byte aligned)
+  float* s_scratch = s_ck + ck_floats;                        // NW x WARP_SCRATCH_FLOATS, 256-byte aligned:
+  s_scratch += ((256u - ((unsigned)__cvta_generic_to_shared(s_scratch) & 255u)) & 255u) >> 2;  // XOR addressing
   unsigned char* s_amask = reinterpret_cast<unsigned char*>(s_scratch + NW * Cfg::WARP_SCRATCH_FLOATS);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -97,9 +107,14 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   }
   __syncthreads();
 
-  float4* pbuf = reinterpret_cast<float4*>(s_scratch + warp * Cfg::WARP_SCRATCH_FLOATS);  // [32][NCHP]
-  float* wbuf = reinterpret_cast<float*>(pbuf + 32 * NCHP);                               // [32][WS]
+  float* wscr = s_scratch + warp * Cfg::WARP_SCRATCH_FLOATS;
+  float* wbuf = wscr + 32 * NCHP * 4;                                     // [32][WS]
+  float2* ybuf = reinterpret_cast<float2*>(wbuf + 32 * WS);               // [2][32 * M]
   const int g = lane / SPW, slot = lane % SPW;  // phase-B role
+  // Dof scratch addressing: chunk c of frame fr lives at float4 position fr * NCHP + (c ^ (fr % NCHP)); with
+  // the scratch aligned to the frame stride that is (address of chunk 0's home) XOR (c * 16): one LOP3.
+  const unsigned pbase = (unsigned)__cvta_generic_to_shared(wscr);
+  const unsigned pa_store = pbase + (unsigned)lane * (NCHP * 16) + ((unsigned)lane & (NCHP - 1)) * 16;
 
   float acc[NA][NDOF];
   float mass[KT];
@@ -116,34 +131,47 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   const int target = sd.target;
   const bool normalize = a.normalize != 0;
 
-  // frames of the first group (lane = frame; lanes past the end re-read the last frame and are masked)
-  float2 y[M];
+  // frames of group `grp` -> stage `st` of this warp's landing zone; frames past the end are zero
+  auto issue_group = [&](int grp, int st) {
+    const float2* gs = src + (long long)grp * 32 * M;
+    float2* d = ybuf + st * (32 * M);
+    const int n = (nt - grp * 32) * M;  // valid elements (may exceed 32 * M)
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const int i = lane + 32 * j;
+      if (i < n)
+        cp_async8(d + i, gs + i);
+      else
+        d[i] = make_float2(0.f, 0.f);
+    }
+    cp_async_commit();
+  };
   int pid = 0;
   if (warp < ngroups) {
-    const int tc = min(warp * 32 + lane, nt - 1);
-#pragma unroll
-    for (int m = 0; m < M; ++m) y[m] = src[(long long)tc * M + m];
-    pid = (int)psrc[tc];
+    issue_group(warp, 0);
+    pid = (int)psrc[min(warp * 32 + lane, nt - 1)];
   }
 
+  int it = 0;
 #pragma unroll 1
-  for (int grp = warp; grp < ngroups; grp += NW) {
+  for (int grp = warp; grp < ngroups; grp += NW, ++it) {
     const int t = grp * 32 + lane;
     const bool valid = t < nt;
-    // prefetch the next group of this warp; it is consumed one iteration later
-    float2 yn[M];
+    // the next group of this warp is fetched while this one is processed
     int pidn = 0;
+    if (grp + NW < ngroups) {
+      issue_group(grp + NW, (it + 1) & 1);
+      pidn = (int)psrc[min((grp + NW) * 32 + lane, nt - 1)];
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    float2 y[M];
     {
-      const int gn = grp + NW;
-      const int tc = min(gn * 32 + lane, nt - 1);
-      if (gn < ngroups) {
+      const float2* ys = ybuf + (it & 1) * (32 * M) + lane * M;
 #pragma unroll
-        for (int m = 0; m < M; ++m) yn[m] = src[(long long)tc * M + m];
-        pidn = (int)psrc[tc];
-      } else {
-#pragma unroll
-        for (int m = 0; m < M; ++m) yn[m] = make_float2(0.f, 0.f);
-      }
+      for (int m = 0; m < M; ++m) y[m] = ys[m];
     }
 
     // ================= phase A: lane = frame =================
@@ -196,8 +224,9 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
       // park this slice's dofs: chunk (gg, c) of frame `lane` at swizzled position (conflict-free both ways)
 #pragma unroll
       for (int c = 0; c < CPG; ++c)
-        pbuf[lane * NCHP + ((gg * CPG + c) ^ (lane & (NCHP - 1)))] =
-            make_float4(pg[4 * c], pg[4 * c + 1], pg[4 * c + 2], pg[4 * c + 3]);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(pa_store ^ (unsigned)((gg * CPG + c) * 16)),
+                     "f"(pg[4 * c]), "f"(pg[4 * c + 1]), "f"(pg[4 * c + 2]), "f"(pg[4 * c + 3])
+                     : "memory");
     }
 
     // Unit normalisation y/(|y|+1e-10) (wpe.hpp:135) scales every class's quadratic form by the same
@@ -269,15 +298,17 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
 #pragma unroll
     for (int step = 0; step < L; ++step) {
       const int fr = step * SPW + slot;
+      const unsigned pa_load =
+          (pbase + (unsigned)fr * (NCHP * 16) + ((unsigned)fr & (NCHP - 1)) * 16) ^ (unsigned)(g * CPG * 16);
       float pv[NDOFP];
 #pragma unroll
-      for (int c = 0; c < CPG; ++c) {
-        const float4 v = pbuf[fr * NCHP + ((g * CPG + c) ^ (fr & (NCHP - 1)))];
-        pv[4 * c] = v.x;
-        pv[4 * c + 1] = v.y;
-        pv[4 * c + 2] = v.z;
-        pv[4 * c + 3] = v.w;
-      }
+      for (int c = 0; c < CPG; ++c)  // (g * CPG + c) ^ x == (g * CPG) ^ c ^ x when CPG is a power of two ...
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(pv[4 * c]), "=f"(pv[4 * c + 1]), "=f"(pv[4 * c + 2]), "=f"(pv[4 * c + 3])
+                     : "r"(CPG_POW2 ? (pa_load ^ (unsigned)(c * 16))
+                                    : ((pbase + (unsigned)fr * (NCHP * 16) + ((unsigned)fr & (NCHP - 1)) * 16) ^
+                                       (unsigned)((g * CPG + c) * 16)))
+                     : "memory");
       float w[WS];
       if (WS == 2) {
         const float2 v = *reinterpret_cast<const float2*>(wbuf + fr * WS);
@@ -310,20 +341,12 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
       }
     }
     __syncwarp();  // the scratch is rewritten by the next group's phase A
-
-#pragma unroll
-    for (int m = 0; m < M; ++m) y[m] = yn[m];
     pid = pidn;
   }
 
-  // ---- reduce: frame slots within the warp, then warps through shared memory
-#pragma unroll
-  for (int o = 1; o < SPW; o <<= 1) {
-#pragma unroll
-    for (int n = 0; n < NA; ++n)
-#pragma unroll
-      for (int j = 0; j < NDOF; ++j) acc[n][j] += __shfl_xor_sync(0xffffffffu, acc[n][j], o);
-  }
+  // ---- reduce. Masses and the likelihood: butterfly over the warp's 32 frame lanes. Accumulators: every
+  // thread parks its tile in shared memory and cell element (g, e) is the sum over the NW * SPW threads that
+  // own slice g, in fixed order.
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
@@ -332,25 +355,42 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   }
   ll *= 0.69314718055994530942;  // back to natural-log units
   __syncthreads();               // every warp is done with its scratch
-  float* red = s_scratch;
-  double* redll = reinterpret_cast<double*>(red + NW * PL::CELL + (NW * PL::CELL & 1));
-  if (slot == 0) {
-    float* r = red + (warp * L + g) * PL::STRIDE;
+  constexpr int DS = Cfg::DUMP_STRIDE;
+  float* dump = s_scratch;                                     // [NW * 32][DS]
+  float* redm = dump + NW * 32 * DS;                           // [NW][KT]
+  double* redll = reinterpret_cast<double*>(redm + ((NW * KT + 1) & ~1));
+  {
+    float* d = dump + tid * DS;
 #pragma unroll
-    for (int n = 0; n < NA; ++n)
+    for (int e4 = 0; e4 < (NA * NDOF + 3) / 4; ++e4) {
+      float v[4];
 #pragma unroll
-      for (int j = 0; j < NDOF; ++j) r[n * NDOF + j] = acc[n][j];
-#pragma unroll
-    for (int k = 0; k < KT; ++k) r[PL::ACC + k] = mass[k];
+      for (int i = 0; i < 4; ++i) {
+        const int e = 4 * e4 + i;
+        v[i] = e < NA * NDOF ? acc[e < NA * NDOF ? e / NDOF : 0][e < NA * NDOF ? e % NDOF : 0] : 0.f;
+      }
+      reinterpret_cast<float4*>(d)[e4] = make_float4(v[0], v[1], v[2], v[3]);
+    }
   }
-  if (lane == 0) redll[warp] = ll;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < KT; ++k) redm[warp * KT + k] = mass[k];
+    redll[warp] = ll;
+  }
   __syncthreads();
   const long long cell = sd.cell_off + (long long)f * sd.nchunks + wi.chunk;
   float* out = a.part + cell * a.cell_stride;
   for (int i = tid; i < PL::CELL; i += kEmThreads) {
+    const int gg = i / PL::STRIDE, e = i - gg * PL::STRIDE;
     float s = 0.f;
+    if (e < PL::ACC) {
+      for (int w = 0; w < NW; ++w)
 #pragma unroll
-    for (int w = 0; w < NW; ++w) s += red[w * PL::CELL + i];
+        for (int sl = 0; sl < SPW; ++sl) s += dump[(w * 32 + gg * SPW + sl) * DS + e];
+    } else {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += redm[w * KT + (e - PL::ACC)];
+    }
     out[i] = s;
   }
   if (tid == 0) {
