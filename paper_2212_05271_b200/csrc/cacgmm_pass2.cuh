@@ -30,6 +30,13 @@ constexpr int pow2_ceil(int x) {
   return p;
 }
 
+/// 8-byte async copy; `valid == false` writes zeros without reading the source (src-size 0).
+__device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(n) : "memory");
+}
+
 template <int M, int L, int KT, bool FINAL>
 struct EmPass2Cfg {
   using Lay = EmLayout<M, L>;
@@ -46,7 +53,8 @@ struct EmPass2Cfg {
   static constexpr int COEF_FLOATS = L * NDOFP * KTP;
   static constexpr int YSTAGE_FLOATS = 32 * M * 2;  // one group of frames (cp.async landing zone)
   // per warp: dof scratch [32][NCHP] float4 | weights [32][WS] | two frame stages; a multiple of 256 bytes
-  static constexpr int WARP_SCRATCH_FLOATS = (32 * NCHP * 4 + 32 * WS + 2 * YSTAGE_FLOATS + 63) & ~63;
+  static constexpr int SUMS = KT + 1;  // per frame lane: class masses and the log-likelihood, kept out of registers
+  static constexpr int WARP_SCRATCH_FLOATS = (32 * NCHP * 4 + 32 * WS + 2 * YSTAGE_FLOATS + 32 * SUMS + 63) & ~63;
   // epilogue dump: every thread parks its accumulators, stride chosen odd in float4 units (conflict-free)
   static constexpr int DUMP_STRIDE = ((NA * NDOF + 3) / 4 | 1) * 4;
   // accumulators + two groups of frames in flight must fit the register file at this occupancy
@@ -110,6 +118,9 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   float* wscr = s_scratch + warp * Cfg::WARP_SCRATCH_FLOATS;
   float* wbuf = wscr + 32 * NCHP * 4;                                     // [32][WS]
   float2* ybuf = reinterpret_cast<float2*>(wbuf + 32 * WS);               // [2][32 * M]
+  float* sums = reinterpret_cast<float*>(ybuf + 2 * 32 * M) + lane;       // [SUMS][32], this lane's column
+#pragma unroll
+  for (int k = 0; k < Cfg::SUMS; ++k) sums[32 * k] = 0.f;
   const int g = lane / SPW, slot = lane % SPW;  // phase-B role
   // Dof scratch addressing: chunk c of frame fr lives at float4 position fr * NCHP + (c ^ (fr % NCHP)); with
   // the scratch aligned to the frame stride that is (address of chunk 0's home) XOR (c * 16): one LOP3.
@@ -117,14 +128,10 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   const unsigned pa_store = pbase + (unsigned)lane * (NCHP * 16) + ((unsigned)lane & (NCHP - 1)) * 16;
 
   float acc[NA][NDOF];
-  float mass[KT];
-#pragma unroll
-  for (int k = 0; k < KT; ++k) mass[k] = 0.f;
 #pragma unroll
   for (int n = 0; n < NA; ++n)
 #pragma unroll
     for (int j = 0; j < NDOF; ++j) acc[n][j] = 0.f;
-  double ll = 0.0;
   float* gout = MODE != kSweepEM && a.gamma != nullptr && sd.g_off >= 0
                     ? a.gamma + sd.g_off + ((long long)f * sd.T + t0) * sd.K
                     : nullptr;
@@ -139,10 +146,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       const int i = lane + 32 * j;
-      if (i < n)
-        cp_async8(d + i, gs + i);
-      else
-        d[i] = make_float2(0.f, 0.f);
+      cp_async8_zfill(d + i, gs + (i < n ? i : 0), i < n);
     }
     cp_async_commit();
   };
@@ -257,12 +261,13 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
     }
     const float rinv = valid ? rcp_approx(se) : 0.f;
     // log2 units, scaled once at the end; the common s^2 factor comes back here: -M log2(s^2) = +M log2(nr2)
-    if (valid) ll += (double)(mx + lg2_approx(se) + (float)M * lg2_approx(nr2));
+    // (a lane sums at most T / 256 such terms in float; lanes and chunks are then summed in double)
+    if (valid) sums[32 * KT] += mx + lg2_approx(se) + (float)M * lg2_approx(nr2);
     float gam[KT];
 #pragma unroll
     for (int k = 0; k < KT; ++k) {
       gam[k] = u[k] * rinv;  // exactly 0 for inactive classes and for lanes past the end
-      mass[k] += gam[k];
+      sums[32 * k] += gam[k];
     }
     if (MODE != kSweepEM) {
       if (gout != nullptr && valid) {
@@ -347,6 +352,10 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   // ---- reduce. Masses and the likelihood: butterfly over the warp's 32 frame lanes. Accumulators: every
   // thread parks its tile in shared memory and cell element (g, e) is the sum over the NW * SPW threads that
   // own slice g, in fixed order.
+  float mass[KT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) mass[k] = sums[32 * k];
+  double ll = (double)sums[32 * KT];
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
