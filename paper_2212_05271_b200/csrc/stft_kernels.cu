@@ -126,6 +126,146 @@ __global__ void __launch_bounds__(kAnaThreads) stft_kernel(StftArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// analyze, n = 512 (the BASELINE configurations): radix-8 x 8 x 8 in registers.
+//
+// 64 threads transform one complex sequence (two real frames, x1 + i x2): every thread holds 8 points, does
+// an 8-point DFT in registers, and the three passes exchange data through 9 KB of shared memory per group
+// (2 exchanges + the final natural-order write: 48 bytes of shared-memory traffic per point, against 360 for
+// the radix-2 form above, which is shared-memory-bandwidth bound). FP64 like the reference (stft.hpp:158-170).
+//
+// Index algebra (W = exp(-2 pi i / 512), n = 64 n2 + 8 n1 + n0, k = k0 + 8 q0 + 64 q1):
+//   pass 1, thread m = 8 n1 + n0 : B[k0]  = sum_n2 x[64 n2 + m] W8^(n2 k0),         times W^(m k0)
+//   pass 2, thread (k0, n0)      : D[q0]  = sum_n1 B[8 n1 + n0][k0] W8^(n1 q0),      times W^(8 n0 q0)
+//   pass 3, thread (k0, q0)      : X[k]   = sum_n0 D[k0][n0][q0] W8^(n0 q1)
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kR8Threads = 256;            // 4 groups of 64
+constexpr int kR8Groups = kR8Threads / 64;
+constexpr int kR8Frames = 4;               // frames per CTA
+constexpr int kR8Xch = 576;                // double2 per group: 8 x 72 (padded) >= 575 (natural order, padded)
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }  // a * (-i)
+
+/// In-register forward 8-point DFT: v[k] <- sum_n v[n] exp(-2 pi i n k / 8).
+__device__ __forceinline__ void dft8(double2 (&v)[8]) {
+  constexpr double h = 0.70710678118654752440;
+  const double2 a0 = cadd(v[0], v[4]), a4 = csub(v[0], v[4]);
+  const double2 a1 = cadd(v[1], v[5]), t5 = csub(v[1], v[5]);
+  const double2 a2 = cadd(v[2], v[6]), a6 = mul_mi(csub(v[2], v[6]));
+  const double2 a3 = cadd(v[3], v[7]), t7 = csub(v[3], v[7]);
+  const double2 a5 = make_double2((t5.x + t5.y) * h, (t5.y - t5.x) * h);    // * W8
+  const double2 a7 = make_double2((t7.y - t7.x) * h, -(t7.x + t7.y) * h);   // * W8^3
+  const double2 b0 = cadd(a0, a2), b2 = csub(a0, a2), b1 = cadd(a1, a3), b3 = mul_mi(csub(a1, a3));
+  const double2 b4 = cadd(a4, a6), b6 = csub(a4, a6), b5 = cadd(a5, a7), b7 = mul_mi(csub(a5, a7));
+  v[0] = cadd(b0, b1);
+  v[4] = csub(b0, b1);
+  v[2] = cadd(b2, b3);
+  v[6] = csub(b2, b3);
+  v[1] = cadd(b4, b5);
+  v[5] = csub(b4, b5);
+  v[3] = cadd(b6, b7);
+  v[7] = csub(b6, b7);
+}
+
+/// v[k] *= w^k, k = 1..7 (powers by recurrence; FP64, far below the final cast to float).
+__device__ __forceinline__ void twiddle8(double2 (&v)[8], double2 w) {
+  double2 p = w;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {
+    v[k] = cmul(v[k], p);
+    if (k < 7) p = cmul(p, w);
+  }
+}
+
+__device__ __forceinline__ void group_sync(int group) {
+  asm volatile("bar.sync %0, 64;" ::"r"(group + 1) : "memory");
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kR8Threads, 2) stft512_kernel(StftArgs a) {
+  extern __shared__ float4 smem_f4[];
+  constexpr int n = 512, F = 257, pad = 256;
+  const int M = a.M;
+  const int run = kR8Frames * M, pitch = run | 1;
+  double2* xch = reinterpret_cast<double2*>(smem_f4);                       // [groups][kR8Xch]
+  double* s_win = reinterpret_cast<double*>(xch + kR8Groups * kR8Xch);      // [512]
+  float2* tile = reinterpret_cast<float2*>(s_win + n);                      // [F][pitch]
+  const SegDev sd = a.segs[blockIdx.y];
+  const int t0 = blockIdx.x * kR8Frames;
+  if (t0 >= sd.T) return;
+  for (int i = threadIdx.x; i < n; i += kR8Threads) s_win[i] = a.win_d[i];
+  __syncthreads();
+  const int group = threadIdx.x >> 6, j = threadIdx.x & 63;
+  const int hi = j >> 3, lo = j & 7;  // pass 2: (k0, n0); pass 3: (k0, q0)
+  const double2 w1 = a.tw_d[j];       // W^m, m = j
+  const double2 w2 = a.tw_d[8 * lo];  // W^(8 n0)
+  double2* xg = xch + group * kR8Xch;
+  const long long N = sd.N;
+  const int npairs = (run + 1) / 2;
+  for (int pair = group; pair < npairs; pair += kR8Groups) {
+    const int s1 = 2 * pair, s2 = s1 + 1;
+    const int tl1 = s1 / M, m1 = s1 % M, tl2 = s2 / M, m2 = s2 % M;
+    const bool v1 = t0 + tl1 < sd.T;
+    const bool v2 = s2 < run && t0 + tl2 < sd.T;
+    const float* x1 = a.audio + sd.audio_off + (long long)m1 * N;
+    const float* x2 = a.audio + sd.audio_off + (long long)m2 * N;
+    const long long b1 = (long long)(t0 + tl1) * a.p.shift - pad;
+    const long long b2 = (long long)(t0 + tl2) * a.p.shift - pad;
+    double2 v[8];
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) {
+      const int i = 64 * n2 + j;
+      const double w = s_win[i];
+      v[n2].x = v1 ? (double)x1[reflect_index(b1 + i, N)] * w : 0.0;
+      v[n2].y = v2 ? (double)x2[reflect_index(b2 + i, N)] * w : 0.0;
+    }
+    dft8(v);
+    twiddle8(v, w1);
+#pragma unroll
+    for (int k0 = 0; k0 < 8; ++k0) xg[k0 * 72 + j] = v[k0];
+    group_sync(group);
+#pragma unroll
+    for (int n1 = 0; n1 < 8; ++n1) v[n1] = xg[hi * 72 + 8 * n1 + lo];
+    dft8(v);
+    twiddle8(v, w2);
+    group_sync(group);  // every thread has read its pass-2 inputs
+#pragma unroll
+    for (int q0 = 0; q0 < 8; ++q0) xg[hi * 72 + q0 * 9 + lo] = v[q0];
+    group_sync(group);
+#pragma unroll
+    for (int n0 = 0; n0 < 8; ++n0) v[n0] = xg[hi * 72 + lo * 9 + n0];
+    dft8(v);
+    group_sync(group);
+    // natural order, padded by one slot per 8 (conflict-free): Z[k] at k + k / 8, k = k0 + 8 q0 + 64 q1
+#pragma unroll
+    for (int q1 = 0; q1 < 8; ++q1) xg[hi + 9 * lo + 72 * q1] = v[q1];
+    group_sync(group);
+    // split the two real transforms (X1 = (Z[f] + conj Z[n-f]) / 2, X2 = (Z[f] - conj Z[n-f]) / 2i)
+    for (int f = j; f < F; f += 64) {
+      const int fn = (n - f) & (n - 1);
+      const double2 zf = xg[f + (f >> 3)], zn = xg[fn + (fn >> 3)];
+      if (v1) tile[f * pitch + s1] = make_float2((float)(0.5 * (zf.x + zn.x)), (float)(0.5 * (zf.y - zn.y)));
+      if (v2) tile[f * pitch + s2] = make_float2((float)(0.5 * (zf.y + zn.y)), (float)(0.5 * (zn.x - zf.x)));
+    }
+    group_sync(group);  // the exchange buffer is rewritten by the next pair
+  }
+  __syncthreads();
+  const int nvalid = min(kR8Frames, sd.T - t0) * M;
+  float2* out = a.y + sd.y_off + (long long)t0 * M;
+  for (int e = threadIdx.x; e < F * nvalid; e += kR8Threads) {
+    const int f = e / nvalid, r = e - f * nvalid;
+    out[(long long)f * sd.T * M + r] = tile[f * pitch + r];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // apply: X(t,f) = sum_c y(f,t,c) * conj(h(f,c)) (beamform.hpp:157-163), written
 // frame-major so the inverse transform reads each frame's bins contiguously.
 // grid (frame tiles of 32, bin tiles of 32, segments), block 32 x 8.
@@ -241,6 +381,15 @@ static int stft_fft_warps(int n) { return std::max(1, std::min(kAnaWarps, 8192 /
 
 cudaError_t launch_stft(const StftArgs& args_in, int nseg, int max_frames, cudaStream_t st) {
   StftArgs a = args_in;
+  if (a.p.fft_size == 512) {
+    const size_t tile = (size_t)a.p.F * ((kR8Frames * a.M) | 1);
+    const size_t smem = sizeof(double2) * kR8Groups * kR8Xch + sizeof(double) * 512 + sizeof(float2) * tile;
+    cudaError_t e = cudaFuncSetAttribute(stft512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((max_frames + kR8Frames - 1) / kR8Frames, nseg);
+    stft512_kernel<<<grid, kR8Threads, smem, st>>>(a);
+    return cudaGetLastError();
+  }
   a.TB = stft_frames_per_cta(a.p.fft_size);
   a.fft_warps = stft_fft_warps(a.p.fft_size);
   const size_t tile_elems = (size_t)a.p.F * ((a.TB * a.M) | 1);
