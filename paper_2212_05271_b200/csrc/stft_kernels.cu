@@ -218,13 +218,36 @@ __global__ void __launch_bounds__(kR8Threads, 2) stft512_kernel(StftArgs a) {
     const float* x2 = a.audio + sd.audio_off + (long long)m2 * N;
     const long long b1 = (long long)(t0 + tl1) * a.p.shift - pad;
     const long long b2 = (long long)(t0 + tl2) * a.p.shift - pad;
+    // all 16 samples of this thread are fetched before any is used; frames that do not touch the signal's
+    // ends (all but a handful per segment) skip the reflection arithmetic (group-uniform branches)
+    float r1[8], r2[8];
+    if (!v1) {
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) r1[n2] = 0.f;
+    } else if (b1 >= 0 && b1 + n <= N) {
+      const float* q = x1 + b1 + j;
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) r1[n2] = q[64 * n2];
+    } else {
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) r1[n2] = x1[reflect_index(b1 + 64 * n2 + j, N)];
+    }
+    if (!v2) {
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) r2[n2] = 0.f;
+    } else if (b2 >= 0 && b2 + n <= N) {
+      const float* q = x2 + b2 + j;
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) r2[n2] = q[64 * n2];
+    } else {
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) r2[n2] = x2[reflect_index(b2 + 64 * n2 + j, N)];
+    }
     double2 v[8];
 #pragma unroll
     for (int n2 = 0; n2 < 8; ++n2) {
-      const int i = 64 * n2 + j;
-      const double w = s_win[i];
-      v[n2].x = v1 ? (double)x1[reflect_index(b1 + i, N)] * w : 0.0;
-      v[n2].y = v2 ? (double)x2[reflect_index(b2 + i, N)] * w : 0.0;
+      const double w = s_win[64 * n2 + j];
+      v[n2] = make_double2((double)r1[n2] * w, (double)r2[n2] * w);
     }
     dft8(v);
     twiddle8(v, w1);
