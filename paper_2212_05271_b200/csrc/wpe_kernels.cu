@@ -18,7 +18,7 @@
 //   wpe_gram_kernel   8x8 complex register tiles, one warp per tile, one lane
 //                     per frame; slab staged channel-major in shared memory
 //   wpe_solve_kernel  FP64 Cholesky of the km x km system per (segment, bin)
-//   wpe_apply_kernel  Y_f = observed - history * conj(G)
+//   wpe_apply2_kernel Y_f = observed - history * conj(G)
 #include "kernels.h"
 
 namespace gssb {
@@ -491,24 +491,33 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Y_f = observed - history * conj(G) (wpe.hpp:95-96). grid (frame tiles, F,
-// segments), block 256: one thread per frame, slab channel-major in shared
-// memory, conj(G) broadcast from shared memory.
+// Y_f = observed - history * conj(G) (wpe.hpp:95-96), two frames per thread, slab channel-major in shared
+// memory, conj(G) broadcast from shared memory. The first version (one frame per thread, an 8-byte filter
+// load per 4 FFMA) issued 88 % of its slots with only 58 % of them FMAs (ncu, profiles/ncu_full_r01.md);
+// here a 16-byte load of two filter entries feeds 16 FFMA. Products and their order per output are unchanged.
+// (Measured and rejected on B200: the packed fma.rn.f32x2 form -- FFMA2 issues no faster than two FFMA here
+// and the operand packing costs extra moves: 6.9 ms against 6.0 ms per cfg2 step.)
+// grid (512-frame tiles, F, segments), block 256.
 // ---------------------------------------------------------------------------
+namespace {
+constexpr int kApplyFrames = 512;
+}  // namespace
+
 template <int M>
-__global__ void __launch_bounds__(256) wpe_apply_kernel(WpeArgs a) {
+__global__ void __launch_bounds__(256) wpe_apply2_kernel(WpeArgs a) {
   extern __shared__ float4 smem_f4[];
   const SegDev sd = a.segs[blockIdx.z];
   if (!sd.wpe_active) return;
-  const int tb = blockIdx.x * 256;
+  const int tb = blockIdx.x * kApplyFrames;
   if (tb >= sd.T) return;
   const int f = blockIdx.y;
   const int taps = a.taps, km = taps * M, H = a.delay + taps - 1;
-  const int SF = 256 + H, pitch = SF | 1;
-  float2* slab = reinterpret_cast<float2*>(smem_f4);   // M * pitch
-  float2* gs = slab + M * pitch;                       // km * M
+  const int SF = kApplyFrames + H, pitch = SF | 1;
+  constexpr int MP = (M + 1) & ~1;                                       // filter row padded to whole float4s
+  float2* gs = reinterpret_cast<float2*>(smem_f4);                       // km * MP
+  float2* slab = gs + km * MP;                                           // M * pitch, channel-major
   const int tid = threadIdx.x;
-  const int nfr = min(256, sd.T - tb);
+  const int nfr = min(kApplyFrames, sd.T - tb);
   const float2* yf = a.yobs + sd.y_off + (long long)f * sd.T * M;
   for (int i = tid; i < (nfr + H) * M; i += 256) {
     const int fr = i / M, c = i - fr * M;
@@ -516,39 +525,58 @@ __global__ void __launch_bounds__(256) wpe_apply_kernel(WpeArgs a) {
     slab[c * pitch + fr] = t >= 0 ? yf[(long long)t * M + c] : make_float2(0.f, 0.f);
   }
   const float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
-  for (int i = tid; i < km * M; i += 256) gs[i] = g[i];
+  for (int i = tid; i < km * MP; i += 256) {
+    const int r = i / MP, c2 = i - r * MP;
+    gs[i] = c2 < M ? g[r * M + c2] : make_float2(0.f, 0.f);
+  }
   __syncthreads();
-  float2 acc[M];
+  float2 acc0[M], acc1[M];
 #pragma unroll
-  for (int c = 0; c < M; ++c) acc[c] = make_float2(0.f, 0.f);
-  const int fi = min(tid, nfr - 1);
+  for (int c = 0; c < M; ++c) acc0[c] = acc1[c] = make_float2(0.f, 0.f);
+  const int f0 = min(tid, nfr - 1), f1 = min(tid + 256, nfr - 1);
   for (int u = 0; u < taps; ++u) {
 #pragma unroll
     for (int c = 0; c < M; ++c) {
-      const float2 v = slab[c * pitch + fi + u];
-      const float2* gr = gs + (u * M + c) * M;
+      const float2 v0 = slab[c * pitch + f0 + u], v1 = slab[c * pitch + f1 + u];
+      const float4* gr = reinterpret_cast<const float4*>(gs + (u * M + c) * MP);
 #pragma unroll
-      for (int c2 = 0; c2 < M; ++c2) {
-        const float2 gg = gr[c2];
-        acc[c2].x = fmaf(v.x, gg.x, acc[c2].x);
-        acc[c2].x = fmaf(-v.y, gg.y, acc[c2].x);
-        acc[c2].y = fmaf(v.x, gg.y, acc[c2].y);
-        acc[c2].y = fmaf(v.y, gg.x, acc[c2].y);
+      for (int p = 0; p < MP / 2; ++p) {
+        const float4 gg = gr[p];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c2 = 2 * p + h;
+          if (c2 < M) {
+            const float gx = h ? gg.z : gg.x, gy = h ? gg.w : gg.y;
+            acc0[c2].x = fmaf(v0.x, gx, acc0[c2].x);
+            acc0[c2].x = fmaf(-v0.y, gy, acc0[c2].x);
+            acc0[c2].y = fmaf(v0.x, gy, acc0[c2].y);
+            acc0[c2].y = fmaf(v0.y, gx, acc0[c2].y);
+            acc1[c2].x = fmaf(v1.x, gx, acc1[c2].x);
+            acc1[c2].x = fmaf(-v1.y, gy, acc1[c2].x);
+            acc1[c2].y = fmaf(v1.x, gy, acc1[c2].y);
+            acc1[c2].y = fmaf(v1.y, gx, acc1[c2].y);
+          }
+        }
       }
     }
   }
-  // observed - s, staged through shared memory for contiguous stores
-  float2 res[M];
+  // observed - prediction, staged through shared memory for contiguous stores
+  float2 res0[M], res1[M];
 #pragma unroll
   for (int c = 0; c < M; ++c) {
-    const float2 o = slab[c * pitch + fi + H];
-    res[c] = make_float2(o.x - acc[c].x, o.y - acc[c].y);
+    const float2 o0 = slab[c * pitch + f0 + H], o1 = slab[c * pitch + f1 + H];
+    res0[c] = make_float2(o0.x - acc0[c].x, o0.y - acc0[c].y);
+    res1[c] = make_float2(o1.x - acc1[c].x, o1.y - acc1[c].y);
   }
   __syncthreads();
-  float2* stage = slab;  // 256 * M <= M * pitch
+  float2* stage = slab;  // 512 * M <= M * pitch
   if (tid < nfr) {
 #pragma unroll
-    for (int c = 0; c < M; ++c) stage[tid * M + c] = res[c];
+    for (int c = 0; c < M; ++c) stage[tid * M + c] = res0[c];
+  }
+  if (tid + 256 < nfr) {
+#pragma unroll
+    for (int c = 0; c < M; ++c) stage[(tid + 256) * M + c] = res1[c];
   }
   __syncthreads();
   float2* out = a.yout + sd.y_off + ((long long)f * sd.T + tb) * M;
@@ -586,12 +614,12 @@ static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F
     dim3 grid(F, nseg);
     wpe_solve_kernel<<<grid, 256, smem, st>>>(a);
   } else {
-    const size_t smem = sizeof(float2) * ((size_t)M * ((256 + H) | 1) + (size_t)km * M);
+    const size_t smem = sizeof(float2) * ((size_t)M * ((kApplyFrames + H) | 1) + (size_t)km * ((M + 1) & ~1));
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(wpe_apply_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(wpe_apply2_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((max_frames + 255) / 256, F, nseg);
-    wpe_apply_kernel<M><<<grid, 256, smem, st>>>(a);
+    dim3 grid((max_frames + kApplyFrames - 1) / kApplyFrames, F, nseg);
+    wpe_apply2_kernel<M><<<grid, 256, smem, st>>>(a);
   }
   return cudaGetLastError();
 }
