@@ -17,7 +17,7 @@
 //   wpe_power_kernel  w_t = 1/lambda_t from the current estimate
 //   wpe_gram_kernel   8x8 complex register tiles, one warp per tile, one lane
 //                     per frame; slab staged channel-major in shared memory
-//   wpe_solve_kernel  FP64 Cholesky of the km x km system per (segment, bin)
+//   wpe_solve2_kernel FP64 Cholesky of the km x km system per (segment, bin)
 //   wpe_apply2_kernel Y_f = observed - history * conj(G)
 #include "kernels.h"
 
@@ -251,69 +251,71 @@ __global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Solve R G = P per (segment, bin) in FP64 (wpe.hpp:90-94; numerics.hpp:32-49,
-// 81-94). grid (F, segments), block 256. Right-looking Cholesky in shared
-// memory, then forward / backward substitution of the M right-hand sides.
+// Solve R G = P per (segment, bin) in FP64 (wpe.hpp:90-94; numerics.hpp:32-49, 81-94): hermitize, regularize,
+// Cholesky, two triangular solves. grid (F, segments), block 128, four blocks per SM.
+//
+// The first version (full square storage, 256 threads, separate forward / backward substitution) spent 55 %
+// of its samples at block barriers (ncu, profiles/ncu_full_r01.md): its serial pieces -- substitution inside
+// a panel by <= 7 threads, one row per thread with a 36-deep dependent FP64 chain in the panel solve -- left
+// 2 resident blocks x 8 warps mostly idle (4.9 ms per cfg2 step; this form: 3.0 ms). What changed:
+//   * packed lower-triangular storage (km(km+1)/2 + M km complex doubles = 48 KB at km = 70): four problems
+//     per SM, so one block's serial sections overlap the others' parallel ones;
+//   * the right-hand sides ride along as M extra rows W = P^H of the matrix being factored: after the last
+//     panel they hold Z^H = (L^-1 P)^H, the forward substitution costs no extra pass;
+//   * each 8 x 8 diagonal block is inverted once by warp 0 (it replaces the block in memory); the panel solve
+//     and the backward substitution become independent dot products of depth <= 8 per output;
+//   * trailing updates split every dot product over two accumulators.
+// A pivot <= 0 fails like Eigen's LLT and takes the eigenvalue-floor fallback (numerics.hpp:58-73, 90-93).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
+namespace {
+constexpr int kSolveThreads = 128;
+constexpr int kPB = 8;
+__device__ __forceinline__ int tri(int i) { return i * (i + 1) / 2; }
+}  // namespace
+
+__global__ void __launch_bounds__(kSolveThreads, 4) wpe_solve2_kernel(WpeArgs a) {
   extern __shared__ float4 smem_f4[];
   const SegDev sd = a.segs[blockIdx.y];
   if (!sd.wpe_active) return;
   const int f = blockIdx.x;
   const int M = a.M, km = a.taps * M, nb = gram_row_blocks(km), ntiles = gram_num_tiles(km, M);
-  const int ld = km + 1;
-  cdbl* A = reinterpret_cast<cdbl*>(smem_f4);  // km x ld
-  cdbl* B = A + (size_t)km * ld;               // km x M
-  double* diag0 = reinterpret_cast<double*>(B + (size_t)km * M);  // regularized diagonal, for the fallback
+  cdbl* Lp = reinterpret_cast<cdbl*>(smem_f4);         // packed lower triangle, row i at tri(i)
+  cdbl* W = Lp + tri(km);                              // M x km: P^H, then Z^H, then X^H
+  cdbl* s_linv = W + (size_t)M * km;                   // kPB x kPB scratch of warp 0
   __shared__ double s_tr;
   __shared__ int s_fail, s_slot;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x, nth = kSolveThreads;
+  const int lane = tid & 31, warp = tid >> 5;
   const float2* tiles = a.gram + (sd.wcell_off + (long long)f * sd.wchunks) * ntiles * kTileElems;
   const long long chunk_stride = (long long)ntiles * kTileElems;
+  const int KMP = (km + 7) & ~7, NR = ((2 * KMP + 16 + 15) / 16) * 16, N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
+  const float* raw = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT);
 
-  if (a.use_tc) {
-    // raw real accumulators of the tensor-core Gram (wpe_gram_tc.cu): D1 = S[0..128) S^T (NR columns),
-    // D2 = S[NR-128..NR) S[128..NR)^T (N2 columns); G(a,b) by symmetry
-    // operand rows: [Re a (KMP)] [Im a (KMP)] [Re y (8)] [Im y (8)], KMP = km rounded up to 8
-    const int KMP = (km + 7) & ~7, NR = ((2 * KMP + 16 + 15) / 16) * 16, N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
-    const float* raw = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT);
-    auto G = [&](int x, int y) -> double {
-      if (x < 128) return (double)raw[x * NCT + y];
-      if (y < 128) return (double)raw[y * NCT + x];
-      return (double)raw[(x - (NR - 128)) * NCT + NR + (y - 128)];
-    };
-    for (int idx = tid; idx < km * km; idx += nth) {
-      const int i = idx / km, j = idx - i * km;
-      if (j > i) continue;
-      const double re = G(i, j) + G(KMP + i, KMP + j);
-      const double im = i == j ? 0.0 : G(KMP + i, j) - G(i, KMP + j);
-      A[i * ld + j] = cd_make(re, im);
-      A[j * ld + i] = cd_make(re, -im);
+  // hermitized R[i][j] (j <= i) and P[i][c] in double from this iteration's Gram (either producer)
+  auto G = [&](int x, int y) -> double {
+    if (x < 128) return (double)raw[x * NCT + y];
+    if (y < 128) return (double)raw[y * NCT + x];
+    return (double)raw[(x - (NR - 128)) * NCT + NR + (y - 128)];
+  };
+  auto load_r = [&](int i, int j) -> cdbl {
+    double re, im;
+    if (a.use_tc) {
+      re = G(i, j) + G(KMP + i, KMP + j);
+      im = G(KMP + i, j) - G(i, KMP + j);
+    } else {
+      const float2* p = tiles + (long long)gram_r_tile(i, j) * kTileElems + (i & 7) * kTC + j % kTC;
+      re = im = 0.0;
+      for (int c = 0; c < sd.wchunks; ++c) {
+        const float2 v = p[c * chunk_stride];
+        re += (double)v.x;
+        im += (double)v.y;
+      }
     }
-    for (int idx = tid; idx < km * M; idx += nth) {
-      const int i = idx / M, c = idx - i * M;
-      B[i * M + c] = cd_make(G(i, 2 * KMP + c) + G(KMP + i, 2 * KMP + 8 + c),
-                             G(KMP + i, 2 * KMP + c) - G(i, 2 * KMP + 8 + c));
-    }
-  } else {
-  // lower triangle of R (upper mirrored by hermitize) and P, summed over chunks in double
-  for (int idx = tid; idx < km * km; idx += nth) {
-    const int i = idx / km, j = idx - i * km;
-    if (j > i) continue;
-    const float2* p = tiles + (long long)gram_r_tile(i, j) * kTileElems + (i & 7) * kTC + j % kTC;
-    double re = 0.0, im = 0.0;
-    for (int c = 0; c < sd.wchunks; ++c) {
-      const float2 v = p[c * chunk_stride];
-      re += (double)v.x;
-      im += (double)v.y;
-    }
-    // hermitize (numerics.hpp:32-38): both triangles come from the same sums
-    if (i == j) im = 0.0;
-    A[i * ld + j] = cd_make(re, im);
-    A[j * ld + i] = cd_make(re, -im);
-  }
-  for (int idx = tid; idx < km * M; idx += nth) {
-    const int i = idx / M, c = idx - i * M;
+    return cd_make(re, i == j ? 0.0 : im);  // hermitize (numerics.hpp:32-38): both triangles from the same sums
+  };
+  auto load_p = [&](int i, int c) -> cdbl {
+    if (a.use_tc)
+      return cd_make(G(i, 2 * KMP + c) + G(KMP + i, 2 * KMP + 8 + c), G(KMP + i, 2 * KMP + c) - G(i, 2 * KMP + 8 + c));
     const float2* p = tiles + (long long)gram_p_tile(i, c, nb, M) * kTileElems + (i & 7) * kTC + c % kTC;
     double re = 0.0, im = 0.0;
     for (int ch = 0; ch < sd.wchunks; ++ch) {
@@ -321,101 +323,148 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
       re += (double)v.x;
       im += (double)v.y;
     }
-    B[i * M + c] = cd_make(re, im);
+    return cd_make(re, im);
+  };
+
+  for (int idx = tid; idx < km * km; idx += nth) {
+    const int i = idx / km, j = idx - i * km;
+    if (j <= i) Lp[tri(i) + j] = load_r(i, j);
   }
+  for (int idx = tid; idx < km * M; idx += nth) {
+    const int i = idx / M, c = idx - i * M;
+    W[c * km + i] = cd_conj(load_p(i, c));
   }
   if (tid == 0) s_fail = 0;
   __syncthreads();
   if (a.debug_rp != nullptr) {  // test hook: expose the assembled Gram
     cdbl* o = a.debug_rp + (long long)f * (km * km + km * M);
-    for (int idx = tid; idx < km * km; idx += nth) o[idx] = A[(idx / km) * ld + idx % km];
-    for (int idx = tid; idx < km * M; idx += nth) o[km * km + idx] = B[idx];
+    for (int idx = tid; idx < km * km; idx += nth) {
+      const int i = idx / km, j = idx - i * km;
+      o[idx] = j <= i ? Lp[tri(i) + j] : cd_conj(Lp[tri(j) + i]);
+    }
+    for (int idx = tid; idx < km * M; idx += nth) o[km * km + idx] = cd_conj(W[(idx % M) * km + idx / M]);
     return;
   }
   if (tid == 0) {  // regularize (numerics.hpp:41-49)
     double tr = 0.0;
-    for (int i = 0; i < km; ++i) tr += A[i * ld + i].re;
+    for (int i = 0; i < km; ++i) tr += Lp[tri(i) + i].re;
     double scale = tr / (double)km;
     if (!(scale > 0.0)) scale = 1.0;
     s_tr = a.regularization * scale;
   }
   __syncthreads();
-  for (int i = tid; i < km; i += nth) {
-    A[i * ld + i].re += s_tr;
-    diag0[i] = A[i * ld + i].re;
-  }
+  for (int i = tid; i < km; i += nth) Lp[tri(i) + i].re += s_tr;
   __syncthreads();
 
-  // Blocked right-looking Cholesky on the lower triangle (panels of PB columns: 3 barriers per panel
-  // instead of 3 per column). A pivot <= 0 fails, Eigen LLT's criterion (numerics.hpp:88).
-  constexpr int PB = 8;
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int kb = 0; kb < km; kb += PB) {
-    const int pb = min(PB, km - kb);
-    if (warp == 0) {  // 1. factor the diagonal block in place
-      cdbl* D = A + kb * ld + kb;
+  // ---- blocked right-looking Cholesky of [R ; W]: A = L L^H, W <- W L^-H. A pivot <= 0 fails (numerics.hpp:88).
+  for (int kb = 0; kb < km; kb += kPB) {
+    const int pb = min(kPB, km - kb);
+    if (warp == 0) {
+      // 1. factor the diagonal block in place, then replace it by its inverse
       bool ok = true;
       for (int k = 0; k < pb; ++k) {
-        const double d = D[k * ld + k].re;
+        cdbl* rowk = Lp + tri(kb + k) + kb;
+        const double d = rowk[k].re;
         if (!(d > 0.0)) {
           ok = false;
           break;  // warp-uniform
         }
-        const double sq = sqrt(d), inv = 1.0 / sq;
+        const double inv = rsqrt(d), sq = d * inv;
         __syncwarp();
-        if (lane == 0) D[k * ld + k] = cd_make(sq, 0.0);
-        if (lane > k && lane < pb) D[lane * ld + k] = cd_scale(D[lane * ld + k], inv);
+        if (lane == 0) rowk[k] = cd_make(sq, 0.0);
+        if (lane > k && lane < pb) {
+          cdbl* e = Lp + tri(kb + lane) + kb + k;
+          *e = cd_scale(*e, inv);
+        }
         __syncwarp();
         const int r = pb - 1 - k;
         if (lane < r * (r + 1) / 2) {
           int ii = 0;
           while ((ii + 1) * (ii + 2) / 2 <= lane) ++ii;
           const int i = k + 1 + ii, jj = k + 1 + (lane - ii * (ii + 1) / 2);
-          D[i * ld + jj] = cd_sub(D[i * ld + jj], cd_mulc(D[i * ld + k], D[jj * ld + k]));
+          cdbl* e = Lp + tri(kb + i) + kb + jj;
+          *e = cd_sub(*e, cd_mulc(Lp[tri(kb + i) + kb + k], Lp[tri(kb + jj) + kb + k]));
         }
         __syncwarp();
       }
-      if (!ok && lane == 0) s_fail = 1;
-    }
-    __syncthreads();
-    if (s_fail) break;
-    const int r0 = kb + pb;  // first row below the panel
-    // 2. panel: row i of L21 solves x L11^H = A[i][kb..kb+pb)
-    for (int i = r0 + tid; i < km; i += nth) {
-      cdbl x[PB];
-#pragma unroll
-      for (int c = 0; c < PB; ++c) {
-        if (c < pb) {
-          cdbl sacc = A[i * ld + kb + c];
-#pragma unroll
-          for (int q = 0; q < PB; ++q)
-            if (q < c) sacc = cd_sub(sacc, cd_mulc(x[q], A[(kb + c) * ld + kb + q]));
-          x[c] = cd_scale(sacc, 1.0 / A[(kb + c) * ld + kb + c].re);
-          A[i * ld + kb + c] = x[c];
+      if (!ok) {
+        if (lane == 0) s_fail = 1;
+      } else {
+        if (lane < pb) {  // column `lane` of L11^-1 by forward substitution
+          const int s0 = lane;
+          for (int r = 0; r < pb; ++r) {
+            cdbl v = cd_make(0.0, 0.0);
+            if (r == s0) {
+              v = cd_make(1.0 / Lp[tri(kb + r) + kb + r].re, 0.0);
+            } else if (r > s0) {
+              cdbl sacc = cd_make(0.0, 0.0);
+              for (int q = s0; q < r; ++q) sacc = cd_add(sacc, cd_mul(Lp[tri(kb + r) + kb + q], s_linv[q * kPB + s0]));
+              v = cd_scale(sacc, -1.0 / Lp[tri(kb + r) + kb + r].re);
+            }
+            s_linv[r * kPB + s0] = v;
+          }
+        }
+        __syncwarp();
+        for (int e = lane; e < pb * pb; e += 32) {
+          const int r = e / pb, c = e - r * pb;
+          if (c <= r) Lp[tri(kb + r) + kb + c] = s_linv[r * kPB + c];
         }
       }
     }
     __syncthreads();
-    // 3. trailing update: A22 -= L21 L21^H (lower triangle)
-    for (int i = r0 + (tid >> 4); i < km; i += 16) {
-      cdbl li[PB];
+    if (s_fail) break;
+    const int r0 = kb + pb;        // first row below the panel
+    const int nbelow = km - r0;    // matrix rows below; the M rows of W follow
+    // 2. panel: row x solves x L11^H = a, i.e. x[c] = sum_{q <= c} a[q] conj(Linv[c][q])
+    for (int t = tid; t < nbelow + M; t += nth) {
+      cdbl* row = t < nbelow ? Lp + tri(r0 + t) + kb : W + (t - nbelow) * km + kb;
+      cdbl av[kPB], x[kPB];
 #pragma unroll
-      for (int c = 0; c < PB; ++c) li[c] = c < pb ? A[i * ld + kb + c] : cd_make(0.0, 0.0);
-      for (int jj = r0 + (tid & 15); jj <= i; jj += 16) {
-        cdbl sacc = A[i * ld + jj];
+      for (int q = 0; q < kPB; ++q) av[q] = q < pb ? row[q] : cd_make(0.0, 0.0);
 #pragma unroll
-        for (int c = 0; c < PB; ++c)
-          if (c < pb) sacc = cd_sub(sacc, cd_mulc(li[c], A[jj * ld + kb + c]));
-        A[i * ld + jj] = sacc;
+      for (int c = 0; c < kPB; ++c) {
+        cdbl sacc = cd_make(0.0, 0.0);
+        if (c < pb) {
+          const cdbl* li = Lp + tri(kb + c) + kb;
+#pragma unroll
+          for (int q = 0; q < kPB; ++q)
+            if (q <= c) sacc = cd_add(sacc, cd_mulc(av[q], li[q]));
+        }
+        x[c] = sacc;
+      }
+#pragma unroll
+      for (int c = 0; c < kPB; ++c)
+        if (c < pb) row[c] = x[c];
+    }
+    __syncthreads();
+    // 3. trailing update: A22 -= L21 L21^H (lower triangle), W2 -= W1 L21^H. Thread grid 8 x 16 over (row, col).
+    {
+      const int ty = tid >> 4, tx = tid & 15;
+      for (int t = ty; t < nbelow + M; t += 8) {
+        const bool isw = t >= nbelow;
+        cdbl* rowi = isw ? W + (t - nbelow) * km : Lp + tri(r0 + t);
+        cdbl li[kPB];
+#pragma unroll
+        for (int c = 0; c < kPB; ++c) li[c] = c < pb ? rowi[kb + c] : cd_make(0.0, 0.0);
+        const int jmax = isw ? km - 1 : r0 + t;  // last column of this row to update
+        for (int jj = r0 + tx; jj <= jmax; jj += 16) {
+          const cdbl* lj = Lp + tri(jj) + kb;
+          cdbl s0 = cd_make(0.0, 0.0), s1 = cd_make(0.0, 0.0);
+#pragma unroll
+          for (int c = 0; c < kPB; c += 2) {
+            if (c < pb) s0 = cd_add(s0, cd_mulc(li[c], lj[c]));
+            if (c + 1 < pb) s1 = cd_add(s1, cd_mulc(li[c + 1], lj[c + 1]));
+          }
+          rowi[jj] = cd_sub(rowi[jj], cd_add(s0, s1));
+        }
       }
     }
     __syncthreads();
   }
+  float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
   if (s_fail) {
     // Eigenvalue-floor fallback (numerics.hpp:58-73, 90-93). Rare: one thread, FP64 cyclic Jacobi in a global
-    // scratch slot. The factorization only touched the lower triangle and the diagonal, so the regularized
-    // matrix is rebuilt from the untouched upper triangle and the saved diagonal; P is still intact.
-    float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
+    // scratch slot; the regularized system is assembled again from the Gram.
     if (tid == 0) {
       const int t = atomicAdd(a.fb_ticket, 1);
       s_slot = t < a.fb_slots ? t : -1;
@@ -429,9 +478,11 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
       double* wv = reinterpret_cast<double*>(Bg + (size_t)km * M);
       for (int idx = tid; idx < km * km; idx += nth) {
         const int i = idx / km, j = idx - i * km;
-        Ag[idx] = i == j ? cd_make(diag0[i], 0.0) : (j > i ? A[i * ld + j] : cd_conj(A[j * ld + i]));
+        cdbl v = j <= i ? load_r(i, j) : cd_conj(load_r(j, i));
+        if (i == j) v.re += s_tr;
+        Ag[idx] = v;
       }
-      for (int idx = tid; idx < km * M; idx += nth) Bg[idx] = B[idx];
+      for (int idx = tid; idx < km * M; idx += nth) Bg[idx] = load_p(idx / M, idx % M);
       __threadfence_block();
       __syncthreads();
       if (tid == 0) s_fail = hermitian_solve(Ag, km, Bg, M, work, work2, wv) == kLinOk ? 2 : 3;
@@ -446,48 +497,41 @@ __global__ void __launch_bounds__(256) wpe_solve_kernel(WpeArgs a) {
     for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2(0.f, 0.f);
     return;
   }
-  // forward: L Z = B, blocked like the factorization (thread c < M owns right-hand side c inside a panel)
-  for (int kb = 0; kb < km; kb += PB) {
-    const int pb = min(PB, km - kb);
-    if (tid < M) {
-      for (int k = 0; k < pb; ++k) {
-        cdbl sacc = B[(kb + k) * M + tid];
-        for (int q = 0; q < k; ++q) sacc = cd_sub(sacc, cd_mul(A[(kb + k) * ld + kb + q], B[(kb + q) * M + tid]));
-        B[(kb + k) * M + tid] = cd_scale(sacc, 1.0 / A[(kb + k) * ld + kb + k].re);
+  // ---- backward: L^H X = Z with W = Z^H, i.e. V = X^H solves V L = W. Panels from the last to the first:
+  // V1 = W1 L11^-1 (the stored inverse), then W[:, j] -= sum_q V1[:, q] L[kb + q][j] for the columns j < kb.
+  for (int kb = ((km - 1) / kPB) * kPB; kb >= 0; kb -= kPB) {
+    const int pb = min(kPB, km - kb);
+    {
+      const int c = tid / kPB, jq = tid % kPB;
+      const bool act = c < M && jq < pb;
+      cdbl v = cd_make(0.0, 0.0);
+      if (act) {
+        const cdbl* wr = W + c * km + kb;
+        for (int q = jq; q < pb; ++q) v = cd_add(v, cd_mul(wr[q], Lp[tri(kb + q) + kb + jq]));
       }
-    }
-    __syncthreads();
-    const int r0 = kb + pb;
-    for (int idx = tid; idx < (km - r0) * M; idx += nth) {
-      const int i = r0 + idx / M, c = idx % M;
-      cdbl sacc = B[i * M + c];
-      for (int q = 0; q < pb; ++q) sacc = cd_sub(sacc, cd_mul(A[i * ld + kb + q], B[(kb + q) * M + c]));
-      B[i * M + c] = sacc;
-    }
-    __syncthreads();
-  }
-  // backward: L^H X = Z
-  for (int kb = ((km - 1) / PB) * PB; kb >= 0; kb -= PB) {
-    const int pb = min(PB, km - kb);
-    if (tid < M) {
-      for (int k = pb - 1; k >= 0; --k) {
-        cdbl sacc = B[(kb + k) * M + tid];
-        for (int q = k + 1; q < pb; ++q) sacc = cd_sub(sacc, cd_cmul(A[(kb + q) * ld + kb + k], B[(kb + q) * M + tid]));
-        B[(kb + k) * M + tid] = cd_scale(sacc, 1.0 / A[(kb + k) * ld + kb + k].re);
-      }
+      __syncwarp();  // a row of W belongs to one warp (kPB divides 32): all its readers are done
+      if (act) W[c * km + kb + jq] = v;
     }
     __syncthreads();
     for (int idx = tid; idx < kb * M; idx += nth) {
-      const int i = idx / M, c = idx % M;
-      cdbl sacc = B[i * M + c];
-      for (int q = 0; q < pb; ++q) sacc = cd_sub(sacc, cd_cmul(A[(kb + q) * ld + i], B[(kb + q) * M + c]));
-      B[i * M + c] = sacc;
+      const int c = idx / kb, j = idx - c * kb;
+      const cdbl* v1 = W + c * km + kb;
+      cdbl s0 = cd_make(0.0, 0.0), s1 = cd_make(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kPB; q += 2) {
+        if (q < pb) s0 = cd_add(s0, cd_mul(v1[q], Lp[tri(kb + q) + j]));
+        if (q + 1 < pb) s1 = cd_add(s1, cd_mul(v1[q + 1], Lp[tri(kb + q + 1) + j]));
+      }
+      W[c * km + j] = cd_sub(W[c * km + j], cd_add(s0, s1));
     }
     __syncthreads();
   }
-  // conj(G) rounded to cfloat (wpe.hpp:95-96)
-  float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
-  for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2((float)B[idx].re, (float)(-B[idx].im));
+  // conj(G) rounded to cfloat (wpe.hpp:95-96): G = X, W = X^H, so conj(G)[i][c] = W[c][i]
+  for (int idx = tid; idx < km * M; idx += nth) {
+    const int i = idx / M, c = idx - i * M;
+    const cdbl v = W[c * km + i];
+    g[idx] = make_float2((float)v.re, (float)v.im);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -607,12 +651,12 @@ static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F
     dim3 grid(ngroups * max_wchunks, F, nseg);
     wpe_gram_kernel<M><<<grid, kGramThreads, smem, st>>>(a);
   } else if (step == 2) {
-    const size_t smem = sizeof(cdbl) * ((size_t)km * (km + 1) + (size_t)km * M) + sizeof(double) * km;
+    const size_t smem = sizeof(cdbl) * ((size_t)km * (km + 1) / 2 + (size_t)km * M + kPB * kPB);
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(wpe_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(wpe_solve2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(F, nseg);
-    wpe_solve_kernel<<<grid, 256, smem, st>>>(a);
+    wpe_solve2_kernel<<<grid, kSolveThreads, smem, st>>>(a);
   } else {
     const size_t smem = sizeof(float2) * ((size_t)M * ((kApplyFrames + H) | 1) + (size_t)km * ((M + 1) & ~1));
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
