@@ -11,7 +11,7 @@
 //   phase A  lane = frame. The lane forms the M^2 Hermitian degrees of freedom ("dofs") of P = y y^H once,
 //            feeds each into the K quadratic forms (coefficients are warp-uniform shared-memory broadcasts),
 //            runs the guide-masked soft-max ONCE per frame without any shuffle, and parks the dofs (float4
-//            chunks, odd frame stride) and the K accumulation weights in the warp's shared-memory scratch.
+//            chunks, XOR-swizzled) and the K accumulation weights in the warp's shared-memory scratch.
 //   phase B  lane = (frame slot, dof slice g of L), the register layout of the accumulators (em_layout.cuh).
 //            Per frame a lane fetches its NDOF dofs as float4s and the weights, and does K * NDOF FMAs.
 //
@@ -44,9 +44,7 @@ struct EmPass2Cfg {
   static constexpr int NDOFP = (NDOF + 3) & ~3;
   static constexpr int CPG = NDOFP / 4;            // float4 chunks per lane slice g
   static constexpr int NCH = L * CPG;              // chunks per frame
-  static constexpr int NCHP = NCH | 1;             // frame stride of the dof scratch (float4 units), odd: the
-                                                   // 8 lanes of a quarter warp (8 frames, same chunk) hit 8
-                                                   // different 16-byte bank groups in both phases
+  static constexpr int NCHP = pow2_ceil(NCH);      // frame stride of the dof scratch (float4 units)
   static constexpr int KTP = KT <= 2 ? 2 : KT <= 4 ? 4 : 8;  // padded class count of the tables
   static constexpr int NA = FINAL ? 2 : KT;
   static constexpr int WS = FINAL ? 2 : KTP;       // weights parked per frame
@@ -75,6 +73,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   using Lay = EmLayout<M, L>;
   constexpr int NDOF = Cfg::NDOF, NDOFP = Cfg::NDOFP, CPG = Cfg::CPG, NCHP = Cfg::NCHP, KTP = Cfg::KTP;
   constexpr int NA = Cfg::NA, WS = Cfg::WS, SPW = Cfg::SPW, NW = Cfg::NW;
+  constexpr bool CPG_POW2 = (CPG & (CPG - 1)) == 0;
   using PL = PartLayout<M, L, KT, NA>;
   extern __shared__ float4 smem_f4[];
   float* s_coef = reinterpret_cast<float*>(smem_f4);          // [g][idx][KTP]
@@ -123,9 +122,10 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
 #pragma unroll
   for (int k = 0; k < Cfg::SUMS; ++k) sums[32 * k] = 0.f;
   const int g = lane / SPW, slot = lane % SPW;  // phase-B role
-  float4* pbuf = reinterpret_cast<float4*>(wscr);          // [32][NCHP]: chunk c of frame fr at fr * NCHP + c
-  float4* pst = pbuf + lane * NCHP;                         // phase A: this lane's frame
-  const float4* pld = pbuf + slot * NCHP + g * CPG;         // phase B: this lane's slice of frame `slot` of a step
+  // Dof scratch addressing: chunk c of frame fr lives at float4 position fr * NCHP + (c ^ (fr % NCHP)); with
+  // the scratch aligned to the frame stride that is (address of chunk 0's home) XOR (c * 16): one LOP3.
+  const unsigned pbase = (unsigned)__cvta_generic_to_shared(wscr);
+  const unsigned pa_store = pbase + (unsigned)lane * (NCHP * 16) + ((unsigned)lane & (NCHP - 1)) * 16;
 
   float acc[NA][NDOF];
 #pragma unroll
@@ -225,10 +225,12 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
           }
         }
       }
-      // park this slice of dofs: chunk (gg, c) of frame `lane`
+      // park this slice's dofs: chunk (gg, c) of frame `lane` at swizzled position (conflict-free both ways)
 #pragma unroll
       for (int c = 0; c < CPG; ++c)
-        pst[gg * CPG + c] = make_float4(pg[4 * c], pg[4 * c + 1], pg[4 * c + 2], pg[4 * c + 3]);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(pa_store ^ (unsigned)((gg * CPG + c) * 16)),
+                     "f"(pg[4 * c]), "f"(pg[4 * c + 1]), "f"(pg[4 * c + 2]), "f"(pg[4 * c + 3])
+                     : "memory");
     }
 
     // Unit normalisation y/(|y|+1e-10) (wpe.hpp:135) scales every class's quadratic form by the same
@@ -301,15 +303,17 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
 #pragma unroll
     for (int step = 0; step < L; ++step) {
       const int fr = step * SPW + slot;
+      const unsigned pa_load =
+          (pbase + (unsigned)fr * (NCHP * 16) + ((unsigned)fr & (NCHP - 1)) * 16) ^ (unsigned)(g * CPG * 16);
       float pv[NDOFP];
 #pragma unroll
-      for (int c = 0; c < CPG; ++c) {
-        const float4 v = pld[step * SPW * NCHP + c];
-        pv[4 * c] = v.x;
-        pv[4 * c + 1] = v.y;
-        pv[4 * c + 2] = v.z;
-        pv[4 * c + 3] = v.w;
-      }
+      for (int c = 0; c < CPG; ++c)  // (g * CPG + c) ^ x == (g * CPG) ^ c ^ x when CPG is a power of two ...
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(pv[4 * c]), "=f"(pv[4 * c + 1]), "=f"(pv[4 * c + 2]), "=f"(pv[4 * c + 3])
+                     : "r"(CPG_POW2 ? (pa_load ^ (unsigned)(c * 16))
+                                    : ((pbase + (unsigned)fr * (NCHP * 16) + ((unsigned)fr & (NCHP - 1)) * 16) ^
+                                       (unsigned)((g * CPG + c) * 16)))
+                     : "memory");
       float w[WS];
       if (WS == 2) {
         const float2 v = *reinterpret_cast<const float2*>(wbuf + fr * WS);
