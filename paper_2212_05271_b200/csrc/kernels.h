@@ -131,7 +131,7 @@ constexpr int em_lanes(int M, int KT) {
   if (M == 5) return KT <= 5 ? 2 : 4;
   if (M == 6) return 4;
   if (M == 7) return KT <= 6 ? 4 : 8;
-  return KT <= 5 ? 4 : 8;
+  return KT <= 3 ? 4 : 8;  // M = 8: 4 lanes put 16 K accumulators + two groups of frames past 128 registers
 }
 /// Class count the kernels are instantiated for (>= K).
 constexpr int em_class_tier(int K) { return K <= 2 ? 2 : K <= 3 ? 3 : K <= 4 ? 4 : K <= 5 ? 5 : K <= 6 ? 6 : 8; }

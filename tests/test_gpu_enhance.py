@@ -127,3 +127,59 @@ def test_resident_batch_matches_one_shot(gss):
     assert ctx.launch_count > 0
     ms = ctx.stage_ms()
     assert ms["mask"] > 0 and ms["stft"] > 0
+
+
+def oracle_unstable_bins(oracle, ss, cfg, threshold=1e-2):
+    """Bins whose masks the ORACLE itself changes by more than `threshold` when its input is perturbed at the
+    FP32 rounding level (x (1 + 1e-7 N(0,1))) or its quadratic form is evaluated in double: 20 EM iterations
+    are chaotic there for any FP32 implementation, the device included (tools/oracle_sensitivity.py)."""
+    ocfg = oracle.stft_cfg(cfg.stft.fft_size, cfg.stft.shift, cfg.stft.window, cfg.stft.sample_rate)
+    y = oracle.stft(ss.audio.channels, ocfg)
+    if cfg.enable_wpe:
+        wc = cfg.wpe
+        y = oracle.wpe(y, oracle.wpe_cfg(wc.taps, wc.delay, wc.iterations, wc.psd_context, wc.regularization))
+    yn = oracle.unit_normalize(y)
+    act = ss.activity
+    base = oracle.em_fit(yn, act.grid, act.target_index, act.noise_index, cfg.bss_iterations).gamma
+    rng = np.random.default_rng(0)
+    pert = (yn * (1.0 + 1e-7 * rng.standard_normal(yn.shape))).astype(np.complex64)
+    unstable = np.zeros(base.shape[0], bool)
+    for other in (oracle.em_fit(pert, act.grid, act.target_index, act.noise_index, cfg.bss_iterations).gamma,
+                  oracle.em_fit(yn, act.grid, act.target_index, act.noise_index, cfg.bss_iterations,
+                                precise_quad=True).gamma):
+        d = np.abs(other - base)
+        unstable |= d.reshape(d.shape[0], -1).max(axis=1) > threshold
+    return unstable
+
+
+def test_enhance_cfg3_shape_ami_8ch_5class(gss, oracle):
+    # BASELINE configs[2]: AMI-shaped, 8 channels, 4 speakers + noise, WPE taps 10 / delay 3, 20 iterations,
+    # 40 s window. Two of the 257 bins (6.6 - 6.9 kHz, almost no speech energy) are chaotic over 20 EM
+    # iterations: the oracle flips their masks under a 1e-7 perturbation of ITS OWN input. The mask and filter
+    # gates are therefore taken over the bins the oracle itself is stable on, every bin on which the device
+    # deviates must be one of the oracle-unstable ones, and those must stay a handful.
+    from paper_2212_05271_b200 import synth
+    w = synth.workload("cfg3", n_segments=1)
+    ss, cfg = w.segments[0], w.cfg
+    got = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
+    want = oracle_enhance(oracle, ss, cfg)
+    assert got.error is None and got.frames == want.frames == 5001
+    assert got.ref_channel == want.ref_channel and got.zeroed_bins == want.zeroed_bins
+    assert [len(o) for o in got.outputs] == [len(o) for o in want.outputs]
+    unstable = oracle_unstable_bins(oracle, ss, cfg)
+    assert unstable.sum() <= 0.02 * len(unstable), int(unstable.sum())
+    dg = np.abs(got.posteriors - want.gamma)
+    per_bin = dg.reshape(dg.shape[0], -1).max(axis=1)
+    deviating = per_bin > 1e-2
+    assert not np.any(deviating & ~unstable), np.nonzero(deviating & ~unstable)[0]
+    s = ~unstable
+    e_gamma = rel_fro(got.posteriors[s], want.gamma[s])
+    p999 = float(np.percentile(dg[s], 99.9))
+    e_h = rel_fro(got.h[s], want.h[s])
+    sdr = sdr_db(got.mono, want.mono)
+    e_ll = abs(got.ll_final - want.ll_final) / abs(want.ll_final)
+    print(f"[cfg3] unstable bins {np.nonzero(unstable)[0].tolist()} rel(gamma)={e_gamma:.2e} p99.9={p999:.2e} "
+          f"rel(h)={e_h:.2e} SDR={sdr:.1f} dB rel(ll)={e_ll:.2e}")
+    assert e_gamma < 1e-3 and p999 < 1e-3 and e_h < 1e-3
+    assert sdr >= 40.0
+    assert e_ll < 1e-4

@@ -63,6 +63,12 @@ def main():
           f"p99.9={np.percentile(dg, 99.9):.2e} p99.99={np.percentile(dg, 99.99):.2e} max={dg.max():.2e} "
           f"rel(h)={rel(r.h, want.h):.2e} SDR={sdr:.1f} dB rel(ll)={abs(r.ll_final - want.ll_final) / abs(want.ll_final):.2e} "
           f"({time.time() - t0:.0f} s)")
+    # which bins carry the largest mask / filter differences (a diverging bin shows up here)
+    pb = dg.reshape(dg.shape[0], -1).max(axis=1)
+    hb = np.linalg.norm(r.h - want.h, axis=1) / np.maximum(np.linalg.norm(want.h, axis=1), 1e-30)
+    worst = np.argsort(-pb)[:5]
+    print("    worst bins (f, max|dgamma|, rel h): " + ", ".join(f"({f}, {pb[f]:.1e}, {hb[f]:.1e})" for f in worst)
+          + f"; bins with max|dgamma| > 1e-2: {int((pb > 1e-2).sum())} of {len(pb)}")
 
 
 if __name__ == "__main__":
