@@ -185,3 +185,16 @@ def test_enhance_cfg3_shape_ami_8ch_5class(gss, oracle):
     # ll_final sums every bin, the two chaotic ones included (they settle in another local optimum): 1e-3 here,
     # 1e-4 on the workloads without such bins
     assert e_ll < 1e-3
+
+
+@pytest.mark.parametrize("channels,speakers,iterations", [(2, 2, 5), (3, 4, 10), (5, 3, 40), (6, 2, 20), (8, 3, 5)])
+def test_enhance_sweep_shapes_channels_and_iterations(gss, oracle, channels, speakers, iterations):
+    # BASELINE configs[4] in miniature: channels 2-8, 2-4 speakers (+ noise), 5-40 EM iterations, WPE on.
+    # Every (M, K) pair takes its own kernel specialisation (lanes per frame, class tier).
+    from paper_2212_05271_b200 import synth
+    from paper_2212_05271_b200.gss import scheduler, stft, wpe
+    cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(10, 2, 3, 0, 1e-10), True,
+                                   iterations)
+    ss = synth.make_supersegment(5000 + 10 * channels + speakers, channels, speakers, 2.0, 1.5, cfg)
+    got = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
+    check_against_oracle(got, oracle_enhance(oracle, ss, cfg), f"sweep M={channels} S={speakers} I={iterations}")
