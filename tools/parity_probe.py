@@ -21,8 +21,15 @@ def rel(a, b):
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "tiny"
-    w = synth.workload(name, n_segments=1)
-    ss, cfg = w.segments[0], w.cfg
+    if name.startswith("custom:"):  # custom:<channels>,<speakers>,<iterations>[,<target seconds>,<context seconds>]
+        from paper_2212_05271_b200.gss import scheduler, stft as st_, wpe as wp_
+        v = [float(x) for x in name.split(":")[1].split(",")]
+        cfg = scheduler.PipelineConfig(st_.StftConfig(512, 128, 0, 16000), wp_.WpeConfig(10, 2, 3, 0, 1e-10), True, int(v[2]))
+        ss = synth.make_supersegment(5000 + 10 * int(v[0]) + int(v[1]), int(v[0]), int(v[1]),
+                                     v[3] if len(v) > 3 else 2.0, v[4] if len(v) > 4 else 1.5, cfg)
+    else:
+        w = synth.workload(name, n_segments=1)
+        ss, cfg = w.segments[0], w.cfg
     ocfg = orc.stft_cfg(cfg.stft.fft_size, cfg.stft.shift, cfg.stft.window, cfg.stft.sample_rate)
     t0 = time.time()
     y_o = orc.stft(ss.audio.channels, ocfg)
