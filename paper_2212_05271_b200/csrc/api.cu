@@ -99,7 +99,7 @@ struct KClock {
     if (b) cudaEventRecord(b, c->stream);
   }
 };
-constexpr int kWpeFallbackSlots = 8;  // concurrent eigenvalue-floor repairs per WPE launch; more is a loud error
+constexpr int kWpeFallbackSlots = 32;  // concurrent eigenvalue-floor repairs per WPE launch; further bins wait for a slot
 enum KernelId { kK_stft = 0, kK_wpe_power, kK_wpe_gram, kK_wpe_solve, kK_wpe_apply, kK_em_pass, kK_em_update,
                 kK_mvdr, kK_apply, kK_istft, kK_misc };
 
@@ -418,7 +418,7 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
       g.gram = m.get<float2>((size_t)o_wcell * wcell);
     g.gconj = m.get<float2>(o_gw);
     g.fb_scratch = m.get<cdbl>((size_t)kWpeFallbackSlots * wpe_fallback_slot_elems(km, M));
-    g.fb_ticket = m.get<int>(1);
+    g.fb_ticket = m.get<int>(kWpeFallbackSlots);  // one busy flag per slot
   }
   if (m.last != cudaSuccess) {
     const std::string why = std::string("device allocation failed: ") + cudaGetErrorString(m.last);
@@ -474,7 +474,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
   a.psd_context = w.psd_context;
   for (int it = 0; it < w.iterations; ++it) {
     a.ycur = it == 0 ? g.Y : g.Yd;
-    CU_TRY(c, cudaMemsetAsync(g.fb_ticket, 0, sizeof(int), c->stream));
+    CU_TRY(c, cudaMemsetAsync(g.fb_ticket, 0, sizeof(int) * kWpeFallbackSlots, c->stream));
     for (int step = 0; step < 4; ++step) {
       KClock k(c, kK_wpe_power + step);
       CU_TRY(c, launch_wpe_step(step, a, g.nseg, g.F, g.max_T, g.max_wchunks, c->stream));

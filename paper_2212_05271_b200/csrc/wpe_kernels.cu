@@ -273,6 +273,142 @@ constexpr int kPB = 8;
 __device__ __forceinline__ int tri(int i) { return i * (i + 1) / 2; }
 }  // namespace
 
+/// X = A^-1 B through the eigenvalue-floor fallback of numerics.hpp:58-73 / :90-93, by the whole block:
+/// parallel-order cyclic Jacobi (round-robin pairing: the n/2 rotations of a round act on disjoint index pairs,
+/// so their column updates, then their row updates, run side by side), eigenvalues floored at 1e-10 of the
+/// largest, X = V diag(1/w) V^H B. A (n x n, full Hermitian, destroyed), V, C (n x nrhs) and w live in a global
+/// scratch slot; `rot` is shared memory for n/2 + 1 rotations (4 complex doubles each) and `red` for the
+/// convergence sums. One thread doing the same (the first version) took 60 ms for a single 40 x 40 bin and
+/// held its whole launch up; this takes about a millisecond. Returns false when no positive finite eigenvalue
+/// exists (SingularMatrixError). Must be called by every thread of the block.
+__device__ bool block_eig_floor_solve(cdbl* A, int n, cdbl* B, int nrhs, cdbl* V, cdbl* C, double* w, cdbl* rot,
+                                      double* red, int tid, int nth) {
+  for (int idx = tid; idx < n * n; idx += nth) V[idx] = cd_make(idx / n == idx % n ? 1.0 : 0.0, 0.0);
+  for (int i = tid; i < n; i += nth) A[i * n + i].im = 0.0;
+  const int np = (n + 1) & ~1, half = np / 2;  // players of the round-robin (an odd n gets a bye)
+  __syncthreads();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int idx = tid; idx < n * n; idx += nth) {
+      const double v = cd_norm(A[idx]);
+      if (idx / n == idx % n) diag += v; else off += v;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      diag += __shfl_xor_sync(0xffffffffu, diag, o);
+    }
+    if ((tid & 31) == 0) {
+      red[2 * (tid >> 5)] = off;
+      red[2 * (tid >> 5) + 1] = diag;
+    }
+    __syncthreads();
+    off = diag = 0.0;
+    for (int wq = 0; wq < nth / 32; ++wq) {
+      off += red[2 * wq];
+      diag += red[2 * wq + 1];
+    }
+    __syncthreads();
+    if (!isfinite(off + diag)) return false;
+    if (off <= 1e-30 * diag || off == 0.0) break;
+    for (int r = 0; r < np - 1; ++r) {
+      // 1. the round's rotations, from the matrix as it stands
+      if (tid < half) {
+        int p = tid == 0 ? np - 1 : (r + tid) % (np - 1);
+        int q = tid == 0 ? r : (r - tid + (np - 1)) % (np - 1);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        cdbl jpp = cd_make(1.0, 0.0), jqp = cd_make(0.0, 0.0), jpq = cd_make(0.0, 0.0), jqq = cd_make(1.0, 0.0);
+        bool act = q < n;
+        if (act) {
+          const cdbl apq = A[p * n + q];
+          const double mag = sqrt(cd_norm(apq));
+          if (mag == 0.0) {
+            act = false;
+          } else {
+            const double app = A[p * n + p].re, aqq = A[q * n + q].re;
+            const cdbl ph = cd_make(apq.re / mag, apq.im / mag);  // e^{i phi}
+            const double tau = (aqq - app) / (2.0 * mag);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            const double c = 1.0 / sqrt(1.0 + t * t), sn = t * c;
+            // J columns: p -> [c ; -s e^{-i phi}], q -> [s ; c e^{-i phi}]
+            jpp = cd_make(c, 0.0);
+            jqp = cd_make(-sn * ph.re, sn * ph.im);
+            jpq = cd_make(sn, 0.0);
+            jqq = cd_make(c * ph.re, -c * ph.im);
+          }
+        }
+        rot[4 * tid] = jpp;
+        rot[4 * tid + 1] = jqp;
+        rot[4 * tid + 2] = jpq;
+        rot[4 * tid + 3] = jqq;
+        reinterpret_cast<int*>(rot + 4 * half)[2 * tid] = act ? p : -1;
+        reinterpret_cast<int*>(rot + 4 * half)[2 * tid + 1] = q;
+      }
+      __syncthreads();
+      const int* pq = reinterpret_cast<const int*>(rot + 4 * half);
+      // 2. A <- A J and V <- V J (disjoint column pairs)
+      for (int it = tid; it < half * n * 2; it += nth) {
+        const int k = it / (2 * n), rem = it - k * 2 * n, i = rem >> 1;
+        const int p = pq[2 * k], q = pq[2 * k + 1];
+        if (p < 0) continue;
+        cdbl* Mx = (rem & 1) ? V : A;
+        const cdbl xp = Mx[i * n + p], xq = Mx[i * n + q];
+        Mx[i * n + p] = cd_add(cd_mul(xp, rot[4 * k]), cd_mul(xq, rot[4 * k + 1]));
+        Mx[i * n + q] = cd_add(cd_mul(xp, rot[4 * k + 2]), cd_mul(xq, rot[4 * k + 3]));
+      }
+      __syncthreads();
+      // 3. A <- J^H A (disjoint row pairs)
+      for (int it = tid; it < half * n; it += nth) {
+        const int k = it / n, j = it - k * n;
+        const int p = pq[2 * k], q = pq[2 * k + 1];
+        if (p < 0) continue;
+        const cdbl apj = A[p * n + j], aqj = A[q * n + j];
+        A[p * n + j] = cd_add(cd_cmul(rot[4 * k], apj), cd_cmul(rot[4 * k + 1], aqj));
+        A[q * n + j] = cd_add(cd_cmul(rot[4 * k + 2], apj), cd_cmul(rot[4 * k + 3], aqj));
+      }
+      __syncthreads();
+      if (tid < half && pq[2 * tid] >= 0) {
+        const int p = pq[2 * tid], q = pq[2 * tid + 1];
+        A[p * n + q] = cd_make(0.0, 0.0);
+        A[q * n + p] = cd_make(0.0, 0.0);
+        A[p * n + p].im = 0.0;
+        A[q * n + q].im = 0.0;
+      }
+      __syncthreads();
+    }
+  }
+  // eigenvalues, floored at 1e-10 of the largest (numerics.hpp:64-72)
+  double emax = -1.0e300;
+  bool finite = true;
+  for (int i = 0; i < n; ++i) {
+    const double v = A[i * n + i].re;
+    finite = finite && isfinite(v);
+    emax = fmax(emax, v);
+  }
+  if (!finite || !(emax > 0.0)) return false;
+  for (int i = tid; i < n; i += nth) w[i] = fmax(A[i * n + i].re, kEigFloorRatio * emax);
+  __syncthreads();
+  for (int idx = tid; idx < n * nrhs; idx += nth) {  // C = diag(1/w) V^H B
+    const int e = idx / nrhs, c = idx - e * nrhs;
+    cdbl sacc = cd_make(0.0, 0.0);
+    for (int j = 0; j < n; ++j) sacc = cd_add(sacc, cd_cmul(V[j * n + e], B[j * nrhs + c]));
+    C[idx] = cd_scale(sacc, 1.0 / w[e]);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * nrhs; idx += nth) {  // X = V C, written over B
+    const int i = idx / nrhs, c = idx - i * nrhs;
+    cdbl sacc = cd_make(0.0, 0.0);
+    for (int e = 0; e < n; ++e) sacc = cd_add(sacc, cd_mul(V[i * n + e], C[e * nrhs + c]));
+    B[idx] = sacc;
+  }
+  __syncthreads();
+  return true;
+}
+
 __global__ void __launch_bounds__(kSolveThreads, 4) wpe_solve2_kernel(WpeArgs a) {
   extern __shared__ float4 smem_f4[];
   const SegDev sd = a.segs[blockIdx.y];
@@ -463,38 +599,47 @@ __global__ void __launch_bounds__(kSolveThreads, 4) wpe_solve2_kernel(WpeArgs a)
   }
   float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
   if (s_fail) {
-    // Eigenvalue-floor fallback (numerics.hpp:58-73, 90-93). Rare: one thread, FP64 cyclic Jacobi in a global
-    // scratch slot; the regularized system is assembled again from the Gram.
+    // Eigenvalue-floor fallback (numerics.hpp:58-73, 90-93). Rare. The block takes one of the launch's global
+    // scratch slots (it waits for one when all are busy: a holder never waits for anybody), assembles the
+    // regularized system again from the Gram and solves it with the block-parallel Jacobi above.
     if (tid == 0) {
-      const int t = atomicAdd(a.fb_ticket, 1);
-      s_slot = t < a.fb_slots ? t : -1;
+      int slot = -1;
+      for (int attempt = 0; slot < 0; ++attempt) {
+        const int cand = (f + attempt) % a.fb_slots;
+        if (atomicCAS(a.fb_ticket + cand, 0, 1) == 0) slot = cand;
+        else if (attempt % a.fb_slots == a.fb_slots - 1) __nanosleep(2000);
+      }
+      s_slot = slot;
     }
     __syncthreads();
-    if (s_slot >= 0) {
-      cdbl* Ag = a.fb_scratch + (size_t)s_slot * wpe_fallback_slot_elems(km, M);
-      cdbl* work = Ag + (size_t)km * km;
-      cdbl* work2 = work + (size_t)km * km;
-      cdbl* Bg = work2 + (size_t)km * km;
-      double* wv = reinterpret_cast<double*>(Bg + (size_t)km * M);
-      for (int idx = tid; idx < km * km; idx += nth) {
-        const int i = idx / km, j = idx - i * km;
-        cdbl v = j <= i ? load_r(i, j) : cd_conj(load_r(j, i));
-        if (i == j) v.re += s_tr;
-        Ag[idx] = v;
-      }
-      for (int idx = tid; idx < km * M; idx += nth) Bg[idx] = load_p(idx / M, idx % M);
-      __threadfence_block();
-      __syncthreads();
-      if (tid == 0) s_fail = hermitian_solve(Ag, km, Bg, M, work, work2, wv) == kLinOk ? 2 : 3;
-      __threadfence_block();
-      __syncthreads();
-      if (s_fail == 2) {
-        for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2((float)Bg[idx].re, (float)(-Bg[idx].im));
-        return;
-      }
+    cdbl* Ag = a.fb_scratch + (size_t)s_slot * wpe_fallback_slot_elems(km, M);
+    cdbl* work = Ag + (size_t)km * km;
+    cdbl* work2 = work + (size_t)km * km;
+    cdbl* Bg = work2 + (size_t)km * km;
+    double* wv = reinterpret_cast<double*>(Bg + (size_t)km * M);
+    for (int idx = tid; idx < km * km; idx += nth) {
+      const int i = idx / km, j = idx - i * km;
+      cdbl v = j <= i ? load_r(i, j) : cd_conj(load_r(j, i));
+      if (i == j) v.re += s_tr;
+      Ag[idx] = v;
     }
-    if (tid == 0) atomicMin(a.status + blockIdx.y, make_status(5, f));
-    for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2(0.f, 0.f);
+    for (int idx = tid; idx < km * M; idx += nth) Bg[idx] = load_p(idx / M, idx % M);
+    __syncthreads();
+    // the factorisation's shared memory is free: rotations and reduction scratch live there
+    cdbl* rot = Lp;
+    double* red = reinterpret_cast<double*>(rot + 4 * ((km + 2) / 2) + (km + 2) / 2 + 2);
+    const bool ok = block_eig_floor_solve(Ag, km, Bg, M, work, work2, wv, rot, red, tid, nth);
+    if (ok) {
+      for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2((float)Bg[idx].re, (float)(-Bg[idx].im));
+    } else {
+      if (tid == 0) atomicMin(a.status + blockIdx.y, make_status(5, f));
+      for (int idx = tid; idx < km * M; idx += nth) g[idx] = make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicExch(a.fb_ticket + s_slot, 0);
+    }
     return;
   }
   // ---- backward: L^H X = Z with W = Z^H, i.e. V = X^H solves V L = W. Panels from the last to the first:

@@ -154,6 +154,27 @@ def test_wpe_eigen_floor_fallback(gss, oracle):
     assert rel_fro(got, want) < 1e-4, rel_fro(got, want)
 
 
+def test_wpe_eigen_floor_fallback_many_bins_at_once(gss, oracle):
+    # every one of 48 bins (more than the 32 scratch slots of a launch) needs the fallback with a 40 x 40
+    # system: the blocks queue for slots instead of failing, and the block-parallel Jacobi keeps it quick
+    import time
+    rng = np.random.RandomState(13)
+    f, t, m, taps = 48, 300, 4, 10
+    s = (rng.randn(f, t, m) + 1j * rng.randn(f, t, m)).astype(np.complex64)
+    y = s.copy()
+    y[:, 3:, :] += 0.4 * s[:, :-3, :]
+    y[:, :, 2] = 0
+    cfg = gss.wpe.WpeConfig(taps, 2, 1, 0, 0.0)
+    gss.wpe.dereverberate(spec(gss, y), cfg)  # warm-up (allocations, module load)
+    t0 = time.perf_counter()
+    got = gss.wpe.dereverberate(spec(gss, y), cfg).data
+    dt = time.perf_counter() - t0
+    want = oracle.wpe(y, oracle.wpe_cfg(taps, 2, 1, 0, 0.0))
+    assert np.isfinite(got).all() and np.all(got[:, :, 2] == 0)
+    assert rel_fro(got, want) < 1e-4, rel_fro(got, want)
+    assert dt < 0.5, dt  # one thread per bin took about 60 ms per 40 x 40 bin
+
+
 # --------------------------------------------------------------------------- cACGMM
 def _em_problem(seed, f, t, m, k, noise=True):
     rng = np.random.RandomState(seed)
