@@ -397,6 +397,142 @@ __global__ void __launch_bounds__(kStftThreads) istft_kernel(IstftArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// synthesize, n = 512: the radix-8 x 8 x 8 register transform of stft512_kernel run backwards (conjugated
+// twiddles, FP32 like istft_kernel), 64 threads per complex transform (two frames ride in one: x_a + i x_b).
+// Overlap-add, window-power normalisation and trimming are istft_kernel's.
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ float2 caddf(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csubf(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 mul_pi(float2 a) { return make_float2(-a.y, a.x); }  // a * (+i)
+
+/// In-register inverse (unscaled) 8-point DFT: v[k] <- sum_n v[n] exp(+2 pi i n k / 8).
+__device__ __forceinline__ void idft8f(float2 (&v)[8]) {
+  constexpr float h = 0.70710678118654752440f;
+  const float2 a0 = caddf(v[0], v[4]), a4 = csubf(v[0], v[4]);
+  const float2 a1 = caddf(v[1], v[5]), t5 = csubf(v[1], v[5]);
+  const float2 a2 = caddf(v[2], v[6]), a6 = mul_pi(csubf(v[2], v[6]));
+  const float2 a3 = caddf(v[3], v[7]), t7 = csubf(v[3], v[7]);
+  const float2 a5 = make_float2((t5.x - t5.y) * h, (t5.x + t5.y) * h);     // * conj(W8)
+  const float2 a7 = make_float2(-(t7.x + t7.y) * h, (t7.x - t7.y) * h);    // * conj(W8)^3
+  const float2 b0 = caddf(a0, a2), b2 = csubf(a0, a2), b1 = caddf(a1, a3), b3 = mul_pi(csubf(a1, a3));
+  const float2 b4 = caddf(a4, a6), b6 = csubf(a4, a6), b5 = caddf(a5, a7), b7 = mul_pi(csubf(a5, a7));
+  v[0] = caddf(b0, b1);
+  v[4] = csubf(b0, b1);
+  v[2] = caddf(b2, b3);
+  v[6] = csubf(b2, b3);
+  v[1] = caddf(b4, b5);
+  v[5] = csubf(b4, b5);
+  v[3] = caddf(b6, b7);
+  v[7] = csubf(b6, b7);
+}
+
+__device__ __forceinline__ void twiddle8f(float2 (&v)[8], float2 w) {
+  float2 p = w;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {
+    v[k] = cmulf(v[k], p);
+    if (k < 7) p = cmulf(p, w);
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kR8Threads) istft512_kernel(IstftArgs a) {
+  extern __shared__ float4 smem_f4[];
+  constexpr int n = 512, F = 257, pad = 256;
+  const int shift = a.p.shift, HB = a.HB;
+  float2* xch = reinterpret_cast<float2*>(smem_f4);                 // [groups][kR8Xch]
+  float* frames = reinterpret_cast<float*>(xch + kR8Groups * kR8Xch);
+  const SegDev sd = a.segs[blockIdx.y];
+  const long long out_len = sd.N;
+  const int R = n / shift;
+  const long long p_lo = (long long)pad + (long long)blockIdx.x * HB * shift;
+  if (p_lo - pad >= out_len) return;
+  const long long h_lo = p_lo / shift;
+  const long long t_first = h_lo - R + 1;
+  const int NF = HB + R - 1;
+  const int group = threadIdx.x >> 6, j = threadIdx.x & 63;
+  const int hi = j >> 3, lo = j & 7;
+  const float2 tw1 = a.tw[j], tw2 = a.tw[8 * lo];                    // exp(-2 pi i k / n): conjugated below
+  const float2 w1 = make_float2(tw1.x, -tw1.y), w2 = make_float2(tw2.x, -tw2.y);
+  float2* xg = xch + group * kR8Xch;
+  const float inv_n = 1.0f / (float)n;
+  const float2* X = a.x + sd.x_off;
+  for (int pair = group; pair < (NF + 1) / 2; pair += kR8Groups) {
+    const int la = 2 * pair, lb = la + 1;
+    const long long ta = t_first + la, tb = t_first + lb;
+    const bool va = ta >= 0 && ta < sd.T;
+    const bool vb = lb < NF && tb >= 0 && tb < sd.T;
+    if (va || vb) {  // group-uniform
+      float2 v[8];
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) {
+        const int k = 64 * n2 + j;           // spectrum index of z = x_a + i x_b
+        const int kk = k <= n / 2 ? k : n - k;
+        const float2 xa = va ? X[ta * F + kk] : make_float2(0.f, 0.f);
+        const float2 xb = vb ? X[tb * F + kk] : make_float2(0.f, 0.f);
+        if (k == 0 || k == n / 2) v[n2] = make_float2(xa.x, xb.x);  // imaginary parts of DC / Nyquist are ignored
+        else if (k < n / 2) v[n2] = make_float2(xa.x - xb.y, xa.y + xb.x);
+        else v[n2] = make_float2(xa.x + xb.y, xb.x - xa.y);          // conj(x_a[n-k]) + i conj(x_b[n-k])
+      }
+      idft8f(v);
+      twiddle8f(v, w1);
+#pragma unroll
+      for (int k0 = 0; k0 < 8; ++k0) xg[k0 * 72 + j] = v[k0];
+      group_sync(group);
+#pragma unroll
+      for (int n1 = 0; n1 < 8; ++n1) v[n1] = xg[hi * 72 + 8 * n1 + lo];
+      idft8f(v);
+      twiddle8f(v, w2);
+      group_sync(group);
+#pragma unroll
+      for (int q0 = 0; q0 < 8; ++q0) xg[hi * 72 + q0 * 9 + lo] = v[q0];
+      group_sync(group);
+#pragma unroll
+      for (int n0 = 0; n0 < 8; ++n0) v[n0] = xg[hi * 72 + lo * 9 + n0];
+      idft8f(v);
+      // sample index i = hi + 8 lo + 64 q1: window, 1/n, split the two frames
+#pragma unroll
+      for (int q1 = 0; q1 < 8; ++q1) {
+        const int i = hi + 8 * lo + 64 * q1;
+        const float w = a.win[i] * inv_n;
+        frames[la * n + i] = va ? v[q1].x * w : 0.f;
+        if (lb < NF) frames[lb * n + i] = vb ? v[q1].y * w : 0.f;
+      }
+      group_sync(group);  // the exchange buffer is rewritten by the next pair
+    } else {
+      for (int i = j; i < n; i += 64) {
+        frames[la * n + i] = 0.f;
+        if (lb < NF) frames[lb * n + i] = 0.f;
+      }
+    }
+  }
+  __syncthreads();
+  float* out = a.wave + sd.wave_off;
+  for (int jj = threadIdx.x; jj < HB * shift; jj += kR8Threads) {
+    const long long p = p_lo + jj;
+    const long long i = p - pad;
+    if (i >= out_len) break;
+    const long long h = p / shift;
+    float acc = 0.f, ws = 0.f;
+    for (int r = R - 1; r >= 0; --r) {  // ascending frame index, as the reference adds them
+      const long long t = h - r;
+      if (t < 0 || t >= sd.T) continue;
+      const int off = (int)(p - t * shift);
+      const float w = a.win[off];
+      acc += frames[(int)(t - t_first) * n + off];
+      ws = fmaf(w, w, ws);
+    }
+    out[i] = ws > 1e-8f ? acc / ws : 0.f;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 static int stft_frames_per_cta(int n) { return n >= 2048 ? 1 : 2048 / n; }
@@ -436,6 +572,16 @@ cudaError_t launch_istft(const IstftArgs& args_in, int nseg, long long max_out_l
   IstftArgs a = args_in;
   a.HB = 16;
   const int R = a.p.fft_size / a.p.shift;
+  if (a.p.fft_size == 512) {
+    const size_t smem = sizeof(float2) * kR8Groups * kR8Xch + sizeof(float) * (size_t)(a.HB + R - 1) * 512;
+    cudaError_t e = cudaFuncSetAttribute(istft512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long per = (long long)a.HB * a.p.shift;
+    dim3 grid((unsigned)((max_out_len + per - 1) / per), nseg);
+    if (grid.x == 0) return cudaSuccess;
+    istft512_kernel<<<grid, kR8Threads, smem, st>>>(a);
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(float2) * (size_t)kStftWarps * a.p.fft_size +
                       sizeof(float) * (size_t)(a.HB + R - 1) * a.p.fft_size;
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
