@@ -493,19 +493,22 @@ __global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweep
 /// Fails (returns false) iff a pivot is <= 0, Eigen LLT's criterion (numerics.hpp:88,105).
 template <int M>
 __device__ __forceinline__ bool warp_cholesky(cdbl* f, int lane) {
+  // lane -> (row, column) of the trailing lower triangle, the same enumeration at every step (found once:
+  // this search inside the step loop was a quarter of the kernel's executed instructions)
+  int ii = 0;
+  while ((ii + 1) * (ii + 2) / 2 <= lane) ++ii;
+  const int jj = lane - ii * (ii + 1) / 2;
   for (int k = 0; k < M; ++k) {
     const double d = f[k * M + k].re;
     if (!(d > 0.0)) return false;  // warp-uniform
-    const double sq = sqrt(d), inv = 1.0 / sq;
+    const double inv = rsqrt(d), sq = d * inv;
     __syncwarp();
     if (lane == 0) f[k * M + k] = cd_make(sq, 0.0);
     if (lane > k && lane < M) f[lane * M + k] = cd_scale(f[lane * M + k], inv);
     __syncwarp();
     const int r = M - 1 - k;
     if (lane < r * (r + 1) / 2) {
-      int ii = 0;
-      while ((ii + 1) * (ii + 2) / 2 <= lane) ++ii;
-      const int i = k + 1 + ii, j = k + 1 + (lane - ii * (ii + 1) / 2);
+      const int i = k + 1 + ii, j = k + 1 + jj;
       f[i * M + j] = cd_sub(f[i * M + j], cd_mulc(f[i * M + k], f[j * M + k]));
     }
     __syncwarp();
