@@ -6,7 +6,7 @@
 // :156-174 (quad_forms), :189-257 (estep_bin), wpe.hpp:124-140 (unit_normalize),
 // numerics.hpp:128-152 (weighted_gram), beamform.hpp:35-85 (accumulate_stats).
 //
-// One EM iteration = em_pass_kernel (E-step + M-step accumulation fused in one
+// One EM iteration = em_pass2_kernel (cacgmm_pass2.cuh: E-step + M-step accumulation fused in one
 // sweep over the spectrogram) + em_update_kernel (per-(f,k) M-step
 // finalisation in FP64: trace normalisation, regularisation, Cholesky inverse,
 // log-det, E-step constants for the next sweep).
@@ -25,26 +25,6 @@
 
 namespace gssb {
 
-/// How the 32 lanes of a warp map to (frame slot, lane-in-frame g) and the shared-memory frame stride
-/// (float2 units), chosen by brute force over the bank model so that the per-lane frame loads of
-/// FramePlan::dofs are (nearly) conflict free:
-///   SPREAD (L <= 4): g = lane / (32/L), slot = lane % (32/L)  -- the L lanes of a frame are 32/L apart
-///   else           : g = lane % L,      slot = lane / L
-template <int M, int L>
-struct LaneMap {
-  static constexpr bool SPREAD = L <= 4;
-  static constexpr int SPW = 32 / L;  // frame slots per warp
-  static constexpr int STRIDE = !SPREAD ? M
-                                : L == 4 ? (M == 7 ? 10 : M == 8 ? 10 : M)
-                                         : (M == 8 ? 9 : M == 6 ? 7 : M == 4 ? 5 : M == 2 ? 3 : M);
-  __device__ static __forceinline__ int g_of(int lane) { return SPREAD ? lane / SPW : lane % L; }
-  __device__ static __forceinline__ int slot_of(int lane) { return SPREAD ? lane % SPW : lane / L; }
-  /// xor offsets that stay inside a frame's lane group / that walk over the slots of a warp
-  static constexpr int G_LO = SPREAD ? SPW : 1, G_HI = SPREAD ? 32 : L;
-  static constexpr int S_LO = SPREAD ? 1 : L, S_HI = SPREAD ? SPW : 32;
-  __device__ static __forceinline__ int lane_of_g(int g) { return SPREAD ? g * SPW : g; }
-};
-
 // ---------------------------------------------------------------------------
 // Per-lane view of one frame
 // ---------------------------------------------------------------------------
@@ -55,13 +35,11 @@ struct FramePlan {
   int offx[Lay::RPL];
   int offz[Lay::RPL][NZ1];
   bool lo[Lay::RPL];
-  float rowmask[Lay::RPL];
 
   __device__ __forceinline__ void init(int g) {
 #pragma unroll
     for (int i = 0; i < Lay::RPL; ++i) {
       int row = g + i * L;
-      rowmask[i] = row < M ? 1.f : 0.f;
       if (row >= M) row = 0;  // idle row: computes finite values that nobody reads
       offx[i] = row;
 #pragma unroll
@@ -90,16 +68,6 @@ struct FramePlan {
         pv[i * M + M - 1] = fmaf(a1, z.x, a2 * z.y);
       }
     }
-  }
-
-  /// |y|^2 of the frame from this lane's diagonal dofs (sum over the L lanes).
-  __device__ __forceinline__ float norm2(const float (&pv)[Lay::NDOF]) const {
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < Lay::RPL; ++i) s = fmaf(rowmask[i], pv[i * M], s);
-#pragma unroll
-    for (int o = LaneMap<M, L>::G_LO; o < LaneMap<M, L>::G_HI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    return s;
   }
 };
 
@@ -134,355 +102,16 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return r;
 }
 
-// Packed FP32 pairs (Blackwell FFMA2): one issue slot for two fused multiply-adds, each rounded exactly like
-// a scalar fma.rn, so results are bit-identical to the scalar form.
-typedef unsigned long long f32x2;
-__device__ __forceinline__ f32x2 pack2(float a, float b) {
-  f32x2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void unpack2(f32x2 v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// ---------------------------------------------------------------------------
-// E-step + accumulation sweep. grid = (work items, F), block = 256.
-// L lanes share a frame; each owns NDOF dofs of P = y y^H, the matching slice
-// of every class's B^-1 (registers) and of every accumulator. Frames stream
-// through a two-stage cp.async pipeline in shared memory.
-//   FINAL = false: accumulators are the KT M-step Grams (weights gamma/q).
-//   FINAL = true : accumulators are the MVDR target / background Grams.
-// ---------------------------------------------------------------------------
-/// B^-1 coefficients live in shared memory ([lane g][class][NDOFP], NDOFP = NDOF rounded up to 4 so a
-/// lane fetches them as float4); that keeps the register tile to the accumulators and lets two CTAs
-/// share an SM when the accumulators are small enough.
 /// Sweep flavours: kSweepEM accumulates the M-step Grams; kSweepEMGamma does the same and may also store
 /// the posteriors (last sweep of the stage entry point); kSweepFinal accumulates the MVDR statistics and
 /// may store the posteriors (last sweep of enhance_batch).
 enum SweepMode { kSweepEM = 0, kSweepEMGamma = 1, kSweepFinal = 2 };
-
-template <int M, int L, int KT, bool FINAL>
-struct EmPassCfg {
-  static constexpr int NDOF = EmLayout<M, L>::NDOF;
-  static constexpr int NDOFP = (NDOF + 3) & ~3;
-  static constexpr int NA = FINAL ? 2 : KT;
-  static constexpr int MINB = (NA * NDOF <= 64) ? 2 : 1;
-  static constexpr int COEF_G = KT * NDOFP + 4;  // per-lane-group stride, skewed by one float4 against bank conflicts
-  static constexpr int COEF_FLOATS = L * COEF_G;
-  static constexpr int FS = LaneMap<M, L>::STRIDE;  // frame stride in the pipeline buffers
-};
-
-template <int M, int L, int KT, int MODE>
-__global__ void __launch_bounds__(kEmThreads, EmPassCfg<M, L, KT, MODE == kSweepFinal>::MINB)
-    em_pass_kernel(EmPassArgs a) {
-  constexpr bool FINAL = MODE == kSweepFinal;
-  using Lay = EmLayout<M, L>;
-  using Cfg = EmPassCfg<M, L, KT, FINAL>;
-  constexpr int NA = FINAL ? 2 : KT;
-  using PL = PartLayout<M, L, KT, NA>;
-  constexpr int NDOF = Lay::NDOF;
-  constexpr int NDOFP = Cfg::NDOFP;
-  constexpr int SLOTS = kEmThreads / L;
-  constexpr int TILE = kEmTileFrames;
-  constexpr int NW = kEmThreads / 32;
-  extern __shared__ float4 smem_f4[];
-  using LM = LaneMap<M, L>;
-  constexpr int FS = Cfg::FS;
-  float2* slab = reinterpret_cast<float2*>(smem_f4);                 // 2 * TILE * FS
-  float* s_coef = reinterpret_cast<float*>(slab + 2 * TILE * FS);    // COEF_FLOATS (16-byte aligned)
-  float* s_ck = s_coef + Cfg::COEF_FLOATS;                           // npat_max * KT
-  unsigned char* s_pat = reinterpret_cast<unsigned char*>(s_ck + a.npat_max * KT);  // 2 * TILE
-  unsigned char* s_amask = s_pat + 2 * TILE;                                        // npat_max: active classes
-
-  const int tid = threadIdx.x;
-  const WorkItem wi = a.work[blockIdx.x];
-  const int f = blockIdx.y;
-  const SegDev sd = a.segs[wi.seg];
-  const int t0 = wi.chunk * sd.TC;
-  const int nt = min(sd.TC, sd.T - t0);
-  const int ntiles = (nt + TILE - 1) / TILE;
-  const float2* src = a.y + sd.y_off + ((long long)f * sd.T + t0) * M;
-  const unsigned char* psrc = a.pat + sd.pat_off + t0;
-
-  auto issue_tile = [&](int tile, int buf) {
-    const int n = min(TILE, nt - tile * TILE) * M;
-    const float2* s = src + (long long)tile * TILE * M;
-    float2* d = slab + buf * TILE * FS;
-    for (int i = tid; i < n; i += kEmThreads) cp_async8(d + (FS == M ? i : (i / M) * FS + i % M), s + i);
-    cp_async_commit();
-  };
-
-  issue_tile(0, 0);
-  {
-    const float* cks = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
-    for (int i = tid; i < sd.npat * KT; i += kEmThreads) s_ck[i] = cks[i];
-    for (int i = tid; i < min(TILE, nt); i += kEmThreads) s_pat[i] = psrc[i];
-    // classes that can be active under a pattern (finite constant); the others have gamma == 0 exactly
-    for (int p = tid; p < sd.npat; p += kEmThreads) {
-      unsigned m = 0;
-      for (int k = 0; k < KT; ++k)
-        if (cks[p * KT + k] != -CUDART_INF_F) m |= 1u << k;
-      s_amask[p] = (unsigned char)m;
-    }
-  }
-
-  const int lane = tid & 31, warp = tid >> 5;
-  const int g = LM::g_of(lane), slot = warp * LM::SPW + LM::slot_of(lane);
-  {
-    const float* cp = a.coef + sd.coef_off + (long long)f * L * (KT * NDOF);
-    for (int i = tid; i < L * KT * NDOFP; i += kEmThreads) {
-      const int j = i % NDOFP, gk = i / NDOFP;
-      s_coef[(gk / KT) * Cfg::COEF_G + (gk % KT) * NDOFP + j] = j < NDOF ? cp[gk * NDOF + j] : 0.f;
-    }
-  }
-  const ulonglong2* c4 = reinterpret_cast<const ulonglong2*>(s_coef + g * Cfg::COEF_G);
-  constexpr int NP = NDOF / 2;            // packed pairs of dofs
-  constexpr bool ODD = (NDOF & 1) != 0;   // + one scalar dof
-  f32x2 acc2[NA][NP > 0 ? NP : 1];
-  float acc1[NA];
-  float mass[KT];
-#pragma unroll
-  for (int k = 0; k < KT; ++k) mass[k] = 0.f;
-#pragma unroll
-  for (int n = 0; n < NA; ++n) {
-    acc1[n] = 0.f;
-#pragma unroll
-    for (int j = 0; j < NP; ++j) acc2[n][j] = 0ull;
-  }
-  double ll = 0.0;
-  FramePlan<M, L> plan;
-  plan.init(g);
-  float* gout = MODE != kSweepEM && a.gamma != nullptr && sd.g_off >= 0
-                    ? a.gamma + sd.g_off + ((long long)f * sd.T + t0) * sd.K
-                    : nullptr;
-  const int target = sd.target;
-  const bool normalize = a.normalize != 0;
-
-  for (int tile = 0; tile < ntiles; ++tile) {
-    const int buf = tile & 1;
-    // prefetch the next tile (data by cp.async, pattern ids through registers)
-    unsigned char pnext[TILE / kEmThreads];
-    const bool more = tile + 1 < ntiles;
-    if (more) {
-      issue_tile(tile + 1, buf ^ 1);
-      const int nn = min(TILE, nt - (tile + 1) * TILE);
-#pragma unroll
-      for (int i = 0; i < TILE / kEmThreads; ++i) {
-        const int idx = tid + i * kEmThreads;
-        pnext[i] = idx < nn ? psrc[(tile + 1) * TILE + idx] : (unsigned char)0;
-      }
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int nin = min(TILE, nt - tile * TILE);
-    const float2* sl = slab + buf * TILE * FS;
-    const unsigned char* sp = s_pat + buf * TILE;
-    // The activity pattern of an iteration's frames (and the classes it can activate) is fetched one
-    // iteration ahead: the LDS -> LDS -> REDUX chain is off the critical path.
-    int pid_n = (int)sp[min(slot, nin - 1)];
-    unsigned am_n = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid_n]);
-    float llf = 0.f;  // this tile's log-likelihood terms (<= TILE / SLOTS of them) in float, folded into ll per tile
-#pragma unroll 1
-    for (int fb = slot; fb < TILE; fb += SLOTS) {
-      if (fb - slot >= nin) break;  // whole stripe of slots is past the data (block-uniform per warp row)
-      const bool valid = fb < nin;
-      const int fbc = valid ? fb : nin - 1;
-      const int pid = pid_n;
-      const unsigned am = am_n;
-      {
-        const int fbn = min(fb + SLOTS, nin - 1);
-        pid_n = (int)sp[fbn];
-        am_n = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid_n]);
-      }
-      float pv[NDOF];
-      plan.dofs(sl + fbc * FS, pv);
-      f32x2 pv2[NP > 0 ? NP : 1];
-#pragma unroll
-      for (int j = 0; j < NP; ++j) pv2[j] = pack2(pv[2 * j], pv[2 * j + 1]);
-      // Classes that are inactive for every frame this warp holds are skipped (warp-uniform branches):
-      // speakers talk in long runs, so a warp's frames usually share one activity pattern.
-      float q[KT];
-#pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        if (am & (1u << k)) {
-          // even dofs accumulate in the low half, odd dofs in the high half (two chains)
-          f32x2 s2 = 0ull;
-          float s1 = 0.f;
-#pragma unroll
-          for (int j4 = 0; j4 < NDOFP / 4; ++j4) {
-            const ulonglong2 c = c4[k * (NDOFP / 4) + j4];
-            if (2 * j4 < NP) s2 = ffma2(c.x, pv2[2 * j4 < NP ? 2 * j4 : 0], s2);
-            if (2 * j4 + 1 < NP) s2 = ffma2(c.y, pv2[2 * j4 + 1 < NP ? 2 * j4 + 1 : 0], s2);
-            if (ODD && (NDOF - 1) / 4 == j4) {  // the scalar tail dof sits in this quad
-              float c0, c1;
-              unpack2(((NDOF - 1) & 2) ? c.y : c.x, c0, c1);
-              s1 = c0 * pv[NDOF - 1];
-            }
-          }
-          float sa, sb;
-          unpack2(s2, sa, sb);
-          q[k] = NP > 0 ? (sa + sb) + s1 : s1;
-        } else {
-          q[k] = 0.f;  // its constant is -inf: the posterior is exactly 0 whatever q is (floored below)
-        }
-      }
-      // One joint butterfly over the frame's L lanes for |y|^2 and every class's partial quadratic form:
-      // the KT + 1 shuffles of a stage are independent, so their latencies overlap.
-      float n2 = 0.f;
-      if (normalize) {
-#pragma unroll
-        for (int i = 0; i < Lay::RPL; ++i) n2 = fmaf(plan.rowmask[i], pv[i * M], n2);
-      }
-#pragma unroll
-      for (int o = LM::G_LO; o < LM::G_HI; o <<= 1) {
-        if (normalize) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-#pragma unroll
-        for (int k = 0; k < KT; ++k) q[k] += __shfl_xor_sync(0xffffffffu, q[k], o);
-      }
-      // Unit normalisation y/(|y|+1e-10) (wpe.hpp:135) scales every class's quadratic form by the same
-      // s^2 = 1/nr2, which cancels in the posteriors and in gamma/q * s^2; only the floor and the likelihood
-      // see it: max(q_raw s^2, 1e-10) = s^2 max(q_raw, 1e-10 nr2).
-      float nr2 = 1.f;
-      if (normalize) {
-        const float nr = sqrt_approx(n2) + 1e-10f;
-        nr2 = nr * nr;
-      }
-      const float qfloor = kQuadFloor * nr2;
-
-      const float* ckp = s_ck + pid * KT;
-      float u[KT];
-      float mx = -CUDART_INF_F;
-#pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        q[k] = fmaxf(q[k], qfloor);                           // cacgmm.hpp:170-171, in raw units
-        // log2 domain: the table holds ck * log2(e); inactive classes carry ck = -inf
-        u[k] = fmaf(-(float)M, lg2_approx(q[k]), ckp[k]);
-        mx = fmaxf(mx, u[k]);
-      }
-      float se = 0.f;
-#pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        u[k] = ex2_approx(u[k] - mx);
-        se += u[k];
-      }
-      const float rinv = valid ? rcp_approx(se) : 0.f;
-      // log2 units, scaled once at the end; the common s^2 factor comes back here: -M log2(s^2) = +M log2(nr2)
-      if (valid && g == 0) llf += mx + lg2_approx(se) + (float)M * lg2_approx(nr2);
-      float gam[KT];
-#pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        gam[k] = u[k] * rinv;  // exactly 0 for inactive classes
-        mass[k] += gam[k];
-        if (MODE != kSweepEM) {
-          if (gout != nullptr && valid && (k % L) == g && k < sd.K)
-            gout[(long long)(tile * TILE + fb) * sd.K + k] = gam[k];
-        }
-      }
-      if (FINAL) {
-        float wt = 0.f, wb = 0.f;
-#pragma unroll
-        for (int k = 0; k < KT; ++k) {
-          wt += (k == target) ? gam[k] : 0.f;
-          wb += (k == target) ? 0.f : gam[k];
-        }
-        const f32x2 wt2 = pack2(wt, wt), wb2 = pack2(wb, wb);
-#pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          acc2[0][j] = ffma2(wt2, pv2[j], acc2[0][j]);
-          acc2[NA - 1][j] = ffma2(wb2, pv2[j], acc2[NA - 1][j]);
-        }
-        if (ODD) {
-          acc1[0] = fmaf(wt, pv[NDOF - 1], acc1[0]);
-          acc1[NA - 1] = fmaf(wb, pv[NDOF - 1], acc1[NA - 1]);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < NA; ++k) {
-          if (am & (1u << k)) {
-            const float w = gam[k] * rcp_approx(q[k]);  // (gamma / q s^2) on the raw frame
-            const f32x2 w2 = pack2(w, w);
-#pragma unroll
-            for (int j = 0; j < NP; ++j) acc2[k][j] = ffma2(w2, pv2[j], acc2[k][j]);
-            if (ODD) acc1[k] = fmaf(w, pv[NDOF - 1], acc1[k]);
-          }
-        }
-      }
-    }
-    ll += (double)llf;
-    __syncthreads();  // everyone is done with buffer `buf` (and with s_pat[buf])
-    if (more) {
-#pragma unroll
-      for (int i = 0; i < TILE / kEmThreads; ++i) s_pat[(buf ^ 1) * TILE + tid + i * kEmThreads] = pnext[i];
-    }
-  }
-
-  // ---- reduce: frame slots within the warp, then warps through shared memory
-  ll = g != 0 ? 0.0 : ll * 0.69314718055994530942;  // back to natural-log units
-  float acc[NA][NDOF];
-#pragma unroll
-  for (int n = 0; n < NA; ++n) {
-#pragma unroll
-    for (int j = 0; j < NP; ++j) unpack2(acc2[n][j], acc[n][2 * j], acc[n][2 * j + 1]);
-    if (ODD) acc[n][NDOF - 1] = acc1[n];
-  }
-#pragma unroll
-  for (int o = LM::S_LO; o < LM::S_HI; o <<= 1) {
-#pragma unroll
-    for (int k = 0; k < KT; ++k) mass[k] += __shfl_xor_sync(0xffffffffu, mass[k], o);
-#pragma unroll
-    for (int n = 0; n < NA; ++n)
-#pragma unroll
-      for (int j = 0; j < NDOF; ++j) acc[n][j] += __shfl_xor_sync(0xffffffffu, acc[n][j], o);
-  }
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) ll += __shfl_xor_sync(0xffffffffu, ll, o);
-  __syncthreads();  // pipeline buffers are free
-  float* red = reinterpret_cast<float*>(smem_f4);
-  double* redll = reinterpret_cast<double*>(red + NW * PL::CELL + (NW * PL::CELL & 1));
-  if (LM::slot_of(lane) == 0) {
-    float* r = red + (warp * L + g) * PL::STRIDE;
-#pragma unroll
-    for (int n = 0; n < NA; ++n)
-#pragma unroll
-      for (int j = 0; j < NDOF; ++j) r[n * NDOF + j] = acc[n][j];
-#pragma unroll
-    for (int k = 0; k < KT; ++k) r[PL::ACC + k] = mass[k];
-  }
-  if (lane == 0) redll[warp] = ll;
-  __syncthreads();
-  const long long cell = sd.cell_off + (long long)f * sd.nchunks + wi.chunk;
-  float* out = a.part + cell * a.cell_stride;
-  for (int i = tid; i < PL::CELL; i += kEmThreads) {
-    float s = 0.f;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) s += red[w * PL::CELL + i];
-    out[i] = s;
-  }
-  if (tid == 0) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) s += redll[w];
-    a.cell_ll[cell] = s;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // M-step finalisation / state preparation. grid = (F, segments), block = KT warps: warp k owns class k

@@ -3,10 +3,10 @@
 // Reference semantics: cacgmm.hpp:156-174 (quad_forms), :189-257 (estep_bin), :308-329 (M-step Gram),
 // wpe.hpp:124-140 (unit_normalize, folded in), beamform.hpp:35-85 (accumulate_stats, last sweep).
 //
-// Why a second design. The first sweep (em_pass_kernel) gives every frame to L lanes and each of them
-// repeats the frame's soft-max, pattern lookup and loop control: at M = 7, K = 4 only 46 % of its issued
-// instructions were FP32 math (ncu, profiles/ncu_full_r01.md). Here a warp works on groups of 32 frames in
-// two phases with different lane maps:
+// Why two phases. The first sweep of this repository gave every frame to L lanes for the whole iteration;
+// each of them repeated the frame's soft-max, pattern lookup and loop control, and at M = 7, K = 4 only 46 %
+// of its issued instructions were FP32 math (25.0 ms per cfg2 step against 16.3 ms for this one; DESIGN.md
+// section 3). Here a warp works on groups of 32 frames in two phases with different lane maps:
 //
 //   phase A  lane = frame. The lane forms the M^2 Hermitian degrees of freedom ("dofs") of P = y y^H once,
 //            feeds each into the K quadratic forms (coefficients are warp-uniform shared-memory broadcasts),
@@ -17,7 +17,7 @@
 //
 // No block-wide barrier in the main loop: each warp streams its own groups of frames (one contiguous run of
 // 32 * M * 8 bytes) through a private two-stage cp.async buffer, and the scratch is private to the warp.
-// Output cells are identical in layout to em_pass_kernel's, so em_update_kernel is shared.
+// Cells (PartLayout) are what em_update_kernel and mvdr_stats_final_kernel read.
 #pragma once
 
 #include "cacgmm_kernels.cuh"
