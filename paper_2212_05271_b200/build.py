@@ -25,7 +25,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--use_fast_math=false"]
 
-CU_SOURCES = ["api.cu", "stft_kernels.cu", "wpe_kernels.cu", "wpe_gram_tc.cu", "beamform_kernels.cu", "cacgmm_dispatch.cu"] + [
+CU_SOURCES = ["api.cu", "stft_kernels.cu", "wpe_kernels.cu", "wpe_gram_tc.cu", "wpe_apply_tc.cu", "beamform_kernels.cu", "cacgmm_dispatch.cu"] + [
     f"cacgmm_m{m}.cu" for m in range(1, 9)]
 CPP_SOURCES = ["host_logic.cpp"]
 HEADERS = ["kernels.h", "gss_internal.cuh", "em_layout.cuh", "linalg.cuh", "cacgmm_kernels.cuh", "cacgmm_pass2.cuh",

@@ -65,6 +65,7 @@ struct gss_b200_ctx {
   double kernel_ms[GSS_B200_NUM_KERNELS] = {0};
   long long kernel_launches[GSS_B200_NUM_KERNELS] = {0};
   int wpe_gram_tc = 1;       // GSS_B200_WPE_GRAM=fp32 selects the FP32-FMA Gram kernel instead of tcgen05
+  int wpe_apply_tc = 1;      // GSS_B200_WPE_APPLY=fp32 selects the FP32-FMA prediction kernel instead of tcgen05
   int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
   int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
 };
@@ -460,6 +461,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
   a.gram = g.gram;
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
+  a.apply_tc = c->wpe_apply_tc && wpe_apply_tc_supported(w.taps, w.delay, g.M);
   a.debug_rp = nullptr;
   a.fb_scratch = g.fb_scratch;
   a.fb_ticket = g.fb_ticket;
@@ -662,6 +664,7 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (const char* s = std::getenv("GSS_B200_WPE_GRAM")) c->wpe_gram_tc = std::strcmp(s, "fp32") != 0;
+  if (const char* s = std::getenv("GSS_B200_WPE_APPLY")) c->wpe_apply_tc = std::strcmp(s, "fp32") != 0;
   if (const char* s = std::getenv("GSS_B200_EM_CHUNK_FRAMES")) c->em_chunk_frames = std::atoi(s);
   if (const char* s = std::getenv("GSS_B200_WPE_CHUNK_FRAMES")) c->wpe_chunk_frames = std::atoi(s);
   *out = c;
@@ -1282,6 +1285,7 @@ gss_status gss_b200_debug_wpe_gram(gss_b200_ctx* c, const float* in, int32_t bin
   a.gram = g.gram;
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
+  a.apply_tc = 0;
   a.debug_rp = d_rp;
   a.fb_scratch = g.fb_scratch;
   a.fb_ticket = g.fb_ticket;

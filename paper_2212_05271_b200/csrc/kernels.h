@@ -54,6 +54,7 @@ struct WpeArgs {
   int fb_slots;
   cdbl* debug_rp;       // non-null: the solve kernel only dumps hermitized R (km x km) and P (km x M) per bin
   int use_tc;           // 1: the Gram of this iteration came from wpe_gram_tc_kernel
+  int apply_tc;         // 1: the prediction runs on the tensor cores (wpe_apply_tc_kernel)
 };
 /// cdbl elements of one scratch slot of the WPE solve's eigenvalue-floor fallback: A, two work matrices, B, eigenvalues
 __host__ __device__ inline int wpe_fallback_slot_elems(int km, int M) { return 3 * km * km + km * M + km / 2 + 1; }
@@ -64,6 +65,9 @@ int wpe_tc_supported(int km, int M);
 int wpe_tc_cell_floats(int km, int M);
 int wpe_tc_rows(int km, int M);
 cudaError_t launch_wpe_gram_tc(const WpeArgs& a, int nseg, int F, cudaStream_t st);
+/// tensor-core prediction (wpe_apply_tc.cu)
+int wpe_apply_tc_supported(int taps, int delay, int M);
+cudaError_t launch_wpe_apply_tc(const WpeArgs& a, int nseg, int F, cudaStream_t st);
 /// one kernel of a WPE iteration; step: 0 power, 1 gram, 2 solve, 3 apply
 cudaError_t launch_wpe_step(int step, const WpeArgs& a, int nseg, int F, int max_frames, int max_wchunks,
                             cudaStream_t st);

@@ -802,6 +802,8 @@ static cudaError_t launch_wpe_step_m(int step, const WpeArgs& a, int nseg, int F
     if (e != cudaSuccess) return e;
     dim3 grid(F, nseg);
     wpe_solve2_kernel<<<grid, kSolveThreads, smem, st>>>(a);
+  } else if (a.apply_tc) {
+    return launch_wpe_apply_tc(a, nseg, F, st);
   } else {
     const size_t smem = sizeof(float2) * ((size_t)M * ((kApplyFrames + H) | 1) + (size_t)km * ((M + 1) & ~1));
     if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;

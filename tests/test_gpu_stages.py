@@ -154,6 +154,34 @@ def test_wpe_eigen_floor_fallback(gss, oracle):
     assert rel_fro(got, want) < 1e-4, rel_fro(got, want)
 
 
+def test_wpe_tensor_core_kernels_match_the_fp32_kernels_at_full_width(gss):
+    # 257 bins x 40 frame tiles keep several blocks per SM busy at once: the tcgen05 Gram and prediction must
+    # agree with the FP32-FMA kernels they replace (a race between a block's workers shows up here, not on the
+    # small shapes above)
+    import os
+    rng = np.random.RandomState(3)
+    f, t, m = 257, 5001, 7
+    s = (rng.randn(f, t, m) + 1j * rng.randn(f, t, m)).astype(np.complex64)
+    y = s.copy()
+    y[:, 3:, :] += 0.5 * s[:, :-3, :]
+    cfg = gss.wpe.WpeConfig(10, 2, 2, 0, 1e-10)
+    got = gss.wpe.dereverberate(spec(gss, y), cfg).data
+    old = {k: os.environ.get(k) for k in ("GSS_B200_WPE_APPLY", "GSS_B200_WPE_GRAM")}
+    os.environ["GSS_B200_WPE_APPLY"] = os.environ["GSS_B200_WPE_GRAM"] = "fp32"
+    try:
+        ctx = gss.Context(0)  # the switches are read when a context is created
+        want = gss.wpe.dereverberate(spec(gss, y), cfg, ctx).data
+        ctx.close()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert rel_fro(got, want) < 1e-5, rel_fro(got, want)
+    assert np.abs(got - want).max() < 1e-3 * np.abs(want).max()
+
+
 def test_wpe_eigen_floor_fallback_many_bins_at_once(gss, oracle):
     # every one of 48 bins (more than the 32 scratch slots of a launch) needs the fallback with a 40 x 40
     # system: the blocks queue for slots instead of failing, and the block-parallel Jacobi keeps it quick
