@@ -135,6 +135,8 @@ def algorithmic_work(segs, cfg):
             nr = (2 * kmp + 16 + 15) // 16 * 16
             nct = nr + max(0, nr - 128)
             w["wpe_gram"]["tensor_flops"] = w["wpe_gram"].get("tensor_flops", 0.0) + J * FT * 3 * 2 * 128 * nct
+            # tensor-core prediction: per frame and tap 2 k-steps of 8, A_hi x [B_hi | B_lo] (N = 32) + A_lo x B_hi (N = 16)
+            w["wpe_apply"]["tensor_flops"] = w["wpe_apply"].get("tensor_flops", 0.0) + J * FT * cfg.wpe.taps * 2 * 2 * 8 * 48
         w["em_pass"]["flops"] += (I + 1) * FT * (3 * M * M + 4 * M * M * K + 20 * K)
         w["em_pass"]["bytes"] += (I + 1) * (8 * FT * M + T * K)
         w["em_update"]["flops"] += (I + 1) * F * K * (8 * M ** 3)
@@ -225,6 +227,7 @@ def run_ours(args, rank, world, local_rank):
         work = algorithmic_work(wl.segments, cfg)
         traffic = _ncu_traffic()
         tc_gram = os.environ.get("GSS_B200_WPE_GRAM", "tc") != "fp32"
+        tc_apply = os.environ.get("GSS_B200_WPE_APPLY", "tc") != "fp32"
         kernels = {}
         for name, (kms_total, n) in kms.items():
             if n == 0 or name not in work:
@@ -247,6 +250,13 @@ def run_ours(args, rank, world, local_rank):
                                       "executed_tensor_tflops": round(ex, 1),
                                       "executed_frac": round(ex / tf32_peak, 4),
                                       "peak_note": "TF32 dense = 0.5 x bf16 " + peak_src})
+            if name == "wpe_apply" and tc_apply and "tensor_flops" in work[name]:
+                ex = work[name]["tensor_flops"] / (per_step * 1e-3) * 1e-12
+                kernels[name].update({"bound": "tensor", "peak": round(tf32_peak, 2), "frac": round(ach / tf32_peak, 4),
+                                      "executed_tensor_tflops": round(ex, 1),
+                                      "executed_frac": round(ex / tf32_peak, 4),
+                                      "peak_note": "TF32 dense = 0.5 x bf16 " + peak_src + "; N = 16-32 MMAs re-stream "
+                                                   "their 128 x 8 A tile from shared memory, which is what bounds them"})
             if name in traffic:
                 kernels[name]["traffic_bytes_per_launch"] = int(traffic[name]["dram_bytes_per_segment_launch"] * nseg)
         top = max(kernels, key=lambda k: kernels[k]["ms_per_step"]) if kernels else None

@@ -14,8 +14,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --c
   $B > gpurun_out/ncu_launch_$tag.log 2>&1
 N="ncu --set full --clock-control none --import-source on"
 timeout 900 $N -k regex:"em_pass" -s 70 -c 2 -o gpurun_out/prof_em_$tag $B > gpurun_out/ncu_em_$tag.log 2>&1
-timeout 900 $N -k regex:"stft512|wpe_" -c 5 -o gpurun_out/prof_wpe_$tag $B > gpurun_out/ncu_wpe_$tag.log 2>&1
+timeout 900 $N -k regex:"^stft512|wpe_" -c 5 -o gpurun_out/prof_wpe_$tag $B > gpurun_out/ncu_wpe_$tag.log 2>&1
 timeout 900 $N -k regex:"em_update" -s 3 -c 1 -o gpurun_out/prof_upd_$tag $B > gpurun_out/ncu_upd_$tag.log 2>&1
-timeout 900 $N -k regex:"beamform_apply|istft_kernel|mvdr_|select_reference" -c 5 -o gpurun_out/prof_tail_$tag $B > gpurun_out/ncu_tail_$tag.log 2>&1
+timeout 900 $N -k regex:"beamform_apply|istft|mvdr_|select_reference" -c 5 -o gpurun_out/prof_tail_$tag $B > gpurun_out/ncu_tail_$tag.log 2>&1
 for w in tiny cfg1 cfg2; do (timeout 300 python tools/parity_probe.py $w) >> gpurun_out/probe_$tag.log 2>&1; done
 tail -3 gpurun_out/test_$tag.log; tail -2 gpurun_out/smoke_$tag.log; tail -c 700 gpurun_out/bench_$tag.log; tail -c 400 gpurun_out/bench_ref_$tag.log

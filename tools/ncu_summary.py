@@ -20,7 +20,7 @@ import re
 import subprocess
 import sys
 
-CLASSES = [("stft", r"^stft"), ("istft", r"^istft_kernel"), ("wpe_power", r"wpe_power"),
+CLASSES = [("stft", r"^stft"), ("istft", r"^istft"), ("wpe_power", r"wpe_power"),
            ("wpe_gram", r"wpe_gram"), ("wpe_solve", r"wpe_solve"), ("wpe_apply", r"wpe_apply"),
            ("em_pass", r"em_pass"), ("em_update", r"em_update_kernel"),
            ("mvdr", r"mvdr_|select_reference"), ("apply", r"beamform_apply"), ("other", r".")]
