@@ -145,21 +145,33 @@ __device__ __forceinline__ bool warp_cholesky(cdbl* f, int lane) {
   return true;
 }
 
-/// inv <- (L L^H)^-1, lane c solves column c (forward then backward substitution).
+/// inv <- (L L^H)^-1, lane c solves column c (forward then backward substitution). The M reciprocals of the
+/// diagonal are taken once (an FP64 division is a ~30-instruction dependent chain; 2 M of them per column sat on
+/// the kernel's critical path) and the loops are unrolled so the factor's entries load ahead of their use.
 template <int M>
 __device__ __forceinline__ void warp_cholesky_inverse(const cdbl* l, cdbl* inv, int lane) {
   if (lane < M) {
     const int c = lane;
+    double rd[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) rd[i] = 1.0 / l[i * M + i].re;
+    cdbl x[M];
+#pragma unroll
     for (int i = 0; i < M; ++i) {
       cdbl s = cd_make(i == c ? 1.0 : 0.0, 0.0);
-      for (int j = 0; j < i; ++j) s = cd_sub(s, cd_mul(l[i * M + j], inv[j * M + c]));
-      inv[i * M + c] = cd_scale(s, 1.0 / l[i * M + i].re);
+#pragma unroll
+      for (int j = 0; j < i; ++j) s = cd_sub(s, cd_mul(l[i * M + j], x[j]));
+      x[i] = cd_scale(s, rd[i]);
     }
+#pragma unroll
     for (int i = M - 1; i >= 0; --i) {
-      cdbl s = inv[i * M + c];
-      for (int j = i + 1; j < M; ++j) s = cd_sub(s, cd_cmul(l[j * M + i], inv[j * M + c]));
-      inv[i * M + c] = cd_scale(s, 1.0 / l[i * M + i].re);
+      cdbl s = x[i];
+#pragma unroll
+      for (int j = i + 1; j < M; ++j) s = cd_sub(s, cd_cmul(l[j * M + i], x[j]));
+      x[i] = cd_scale(s, rd[i]);
     }
+#pragma unroll
+    for (int i = 0; i < M; ++i) inv[i * M + c] = x[i];
   }
   __syncwarp();
 }
