@@ -268,10 +268,10 @@ int pick_chunks(gss_b200_ctx* c, int T, long long ctas_one_chunk) {
   int nch = 1;
   if (c->em_chunk_frames > 0) {
     nch = (T + c->em_chunk_frames - 1) / c->em_chunk_frames;
-  } else if (ctas_one_chunk < 2 * 148) {
-    // one segment alone should still fill the 148 SMs (2 CTAs each); every extra chunk costs a sweep prologue
-    // and a cell reduction per (segment, bin)
-    const int want = (int)((2 * 148 + ctas_one_chunk - 1) / ctas_one_chunk);
+  } else if (ctas_one_chunk < 148) {
+    // one segment alone should still put a block on each of the 148 SMs; every extra chunk costs a sweep
+    // prologue and a cell reduction per (segment, bin) (two half-length blocks per SM take as long as one)
+    const int want = (int)((148 + ctas_one_chunk - 1) / ctas_one_chunk);
     nch = std::max(1, std::min(want, (T + 255) / 256));
   }
   int TC = (T + nch - 1) / nch;
