@@ -176,6 +176,133 @@ __device__ __forceinline__ void warp_cholesky_inverse(const cdbl* l, cdbl* inv, 
   __syncwarp();
 }
 
+/// Eigenvalue-floor inverse and log-determinant (numerics.hpp:58-73, 103-122) by a whole warp, for the shape
+/// matrices Cholesky rejects (rank-deficient classes in the later EM iterations: one such bin, solved by one
+/// lane, used to hold its launch up for ~300 us). Two-sided Jacobi with the round-robin pairing: the (M+1)/2
+/// rotations of a round touch disjoint row / column pairs and are applied by all lanes at once.
+/// b: input (lower triangle read); a: scratch, receives the inverse; v: scratch (eigenvectors); rot: 4 cdbl +
+/// 2 ints per pair. Returns false (warp-uniform) on non-finite values or when no eigenvalue is positive.
+template <int M>
+__device__ __noinline__ bool warp_eig_floor_inverse(const cdbl* b, cdbl* a, cdbl* v, cdbl* rot, double* log_det,
+                                                    int lane) {
+  constexpr int MM = M * M, NP = (M + 1) & ~1, HALF = NP / 2;
+  for (int e = lane; e < MM; e += 32) {
+    const int i = e / M, j = e - i * M;
+    cdbl x = i >= j ? b[i * M + j] : cd_conj(b[j * M + i]);
+    if (i == j) x.im = 0.0;
+    a[e] = x;
+    v[e] = cd_make(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncwarp();
+  int* pq = reinterpret_cast<int*>(rot + 4 * HALF);
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int e = lane; e < MM; e += 32) {
+      const double n2 = cd_norm(a[e]);
+      if (e / M == e % M) diag += n2; else off += n2;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      diag += __shfl_xor_sync(0xffffffffu, diag, o);
+    }
+    if (!isfinite(off + diag)) return false;
+    if (off <= 1e-30 * diag || off == 0.0) break;
+    for (int r = 0; r < NP - 1; ++r) {
+      if (lane < HALF) {  // this round's rotations, from the matrix as it stands
+        int p = lane == 0 ? NP - 1 : (r + lane) % (NP - 1);
+        int q = lane == 0 ? r : (r - lane + (NP - 1)) % (NP - 1);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        cdbl jpp = cd_make(1.0, 0.0), jqp = cd_make(0.0, 0.0), jpq = cd_make(0.0, 0.0), jqq = cd_make(1.0, 0.0);
+        bool act = q < M;
+        if (act) {
+          const cdbl apq = a[p * M + q];
+          const double mag = sqrt(cd_norm(apq));
+          if (mag == 0.0) {
+            act = false;
+          } else {
+            const double app = a[p * M + p].re, aqq = a[q * M + q].re;
+            const cdbl ph = cd_make(apq.re / mag, apq.im / mag);  // e^{i phi}
+            const double tau = (aqq - app) / (2.0 * mag);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            const double c = 1.0 / sqrt(1.0 + t * t), sn = t * c;
+            // J columns: p -> [c ; -s e^{-i phi}], q -> [s ; c e^{-i phi}]
+            jpp = cd_make(c, 0.0);
+            jqp = cd_make(-sn * ph.re, sn * ph.im);
+            jpq = cd_make(sn, 0.0);
+            jqq = cd_make(c * ph.re, -c * ph.im);
+          }
+        }
+        rot[4 * lane] = jpp;
+        rot[4 * lane + 1] = jqp;
+        rot[4 * lane + 2] = jpq;
+        rot[4 * lane + 3] = jqq;
+        pq[2 * lane] = act ? p : -1;
+        pq[2 * lane + 1] = q;
+      }
+      __syncwarp();
+      for (int it = lane; it < HALF * M * 2; it += 32) {  // A <- A J, V <- V J (disjoint column pairs)
+        const int k = it / (2 * M), rem = it - k * 2 * M, i = rem >> 1;
+        const int p = pq[2 * k], q = pq[2 * k + 1];
+        if (p < 0) continue;
+        cdbl* mx = (rem & 1) ? v : a;
+        const cdbl xp = mx[i * M + p], xq = mx[i * M + q];
+        mx[i * M + p] = cd_add(cd_mul(xp, rot[4 * k]), cd_mul(xq, rot[4 * k + 1]));
+        mx[i * M + q] = cd_add(cd_mul(xp, rot[4 * k + 2]), cd_mul(xq, rot[4 * k + 3]));
+      }
+      __syncwarp();
+      for (int it = lane; it < HALF * M; it += 32) {  // A <- J^H A (disjoint row pairs)
+        const int k = it / M, j = it - k * M;
+        const int p = pq[2 * k], q = pq[2 * k + 1];
+        if (p < 0) continue;
+        const cdbl apj = a[p * M + j], aqj = a[q * M + j];
+        a[p * M + j] = cd_add(cd_cmul(rot[4 * k], apj), cd_cmul(rot[4 * k + 1], aqj));
+        a[q * M + j] = cd_add(cd_cmul(rot[4 * k + 2], apj), cd_cmul(rot[4 * k + 3], aqj));
+      }
+      __syncwarp();
+      if (lane < HALF && pq[2 * lane] >= 0) {
+        const int p = pq[2 * lane], q = pq[2 * lane + 1];
+        a[p * M + q] = cd_make(0.0, 0.0);
+        a[q * M + p] = cd_make(0.0, 0.0);
+        a[p * M + p].im = 0.0;
+        a[q * M + q].im = 0.0;
+      }
+      __syncwarp();
+    }
+  }
+  double w[M], emax = -1.0e300;
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    w[i] = a[i * M + i].re;
+    finite = finite && isfinite(w[i]);
+    emax = fmax(emax, w[i]);
+  }
+  if (!finite || !(emax > 0.0)) return false;
+  double ld = 0.0;
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    w[i] = fmax(w[i], kEigFloorRatio * emax);
+    ld += log(w[i]);
+    w[i] = 1.0 / w[i];
+  }
+  __syncwarp();  // every lane holds the eigenvalues: a can take the inverse V diag(1/w) V^H
+  for (int e = lane; e < MM; e += 32) {
+    const int i = e / M, j = e - i * M;
+    cdbl s = cd_make(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < M; ++q) s = cd_add(s, cd_scale(cd_mulc(v[i * M + q], v[j * M + q]), w[q]));
+    a[e] = s;
+  }
+  __syncwarp();
+  *log_det = ld;
+  return true;
+}
+
 template <int M, int L, int KT>
 __global__ void __launch_bounds__(KT * 32) em_update_kernel(EmUpdateArgs a) {
   using Lay = EmLayout<M, L>;
@@ -183,6 +310,7 @@ __global__ void __launch_bounds__(KT * 32) em_update_kernel(EmUpdateArgs a) {
   constexpr int NDOF = Lay::NDOF;
   constexpr int MM = M * M;
   __shared__ cdbl s_b[KT][MM], s_f[KT][MM], s_inv[KT][MM];
+  __shared__ cdbl s_rot[KT][5 * ((M + 1) / 2)];  // the fallback's rotations: 4 cdbl + 2 ints per pair
   __shared__ double s_pi[KT], s_ld[KT];
 
   const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -270,9 +398,13 @@ __global__ void __launch_bounds__(KT * 32) em_update_kernel(EmUpdateArgs a) {
         for (int i = 0; i < M; ++i) pd *= F[i * M + i].re;
         my_ld = 2.0 * log(pd);
         warp_cholesky_inverse<M>(F, inv, lane);
+      } else if (warp_eig_floor_inverse<M>(B, F, inv, s_rot[k], &my_ld, lane)) {
+        // eigenvalue-floor fallback (numerics.hpp:103-122), whole warp; the inverse is left in F
+        for (int e = lane; e < MM; e += 32) inv[e] = F[e];
+        __syncwarp();
       } else {
-        // rare path, one lane: eigenvalue-floor fallback, then the retry on regularize(B)
-        // (numerics.hpp:103-122, cacgmm.hpp:134-140)
+        // no usable eigenvalue: one lane repeats the decomposition and then retries on regularize(B)
+        // (cacgmm.hpp:134-140); practically never taken
         __syncwarp();
         if (lane == 0) {
           cdbl fact[MM], work[MM], linv[MM];

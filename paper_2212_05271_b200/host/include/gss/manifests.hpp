@@ -301,7 +301,7 @@ class JsonReader {
     ++i_;
     return out;
   }
-  const std::string& s_;
+  const std::string s_;  // a copy: callers pass temporaries
   size_t i_ = 0;
 };
 

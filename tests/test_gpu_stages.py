@@ -278,6 +278,35 @@ def test_em_dead_class_and_errors(gss, oracle):
         gss.cacgmm.em_fit(spec(gss, yn), bad, 2)
 
 
+@pytest.mark.parametrize("m", [2, 4, 7, 8])
+def test_em_shape_matrices_cholesky_rejects_take_the_eigenvalue_floor(gss, oracle, m):
+    # cacgmm.hpp:134-140 / numerics.hpp:103-122: an indefinite or rank-deficient shape matrix is inverted through
+    # the eigenvalue floor (1e-10 * lambda_max). On the device that is a warp-parallel Jacobi; it must agree with
+    # the oracle's fallback through the likelihood and the posteriors' normaliser.
+    f, t, k = 9, 300, 3
+    y, act = _em_problem(31 + m, f, t, m, k, True)
+    yn = oracle.unit_normalize(y)
+    rng = np.random.RandomState(m)
+    shapes = np.zeros((f, k, m, m), np.complex128)
+    for ff in range(f):
+        for kk in range(k):
+            q, _ = np.linalg.qr(rng.randn(m, m) + 1j * rng.randn(m, m))
+            w = rng.uniform(0.5, 2.0, m)
+            kind = (ff + kk) % 3
+            if kind == 0 and m > 1:
+                w[rng.randint(m)] = -0.3            # indefinite
+            elif kind == 1:
+                w[: max(1, m // 2)] = -1e-7         # rank-deficient up to rounding (an exact zero pivot may come
+                #                                     out as +-1e-17 and pass one Cholesky but not the other)
+            b = (q * w) @ q.conj().T                # kind 2: positive definite (the Cholesky path, same launch)
+            shapes[ff, kk] = 0.5 * (b + b.conj().T)
+    pi = rng.uniform(0.2, 1.0, (f, k))
+    am = gss.manifests.ActivityMatrix(act, ["c%d" % i for i in range(k)], 0, k - 1)
+    got = gss.cacgmm.log_likelihood(spec(gss, yn), gss.cacgmm.CacgmmState(pi, shapes), am)
+    want = oracle.log_likelihood(yn, act, pi, shapes, k - 1)
+    assert np.isfinite(got) and abs(got - want) / abs(want) < 2e-5, (got, want)
+
+
 def test_em_degenerate_frames_without_noise_class(gss, oracle):
     # frames with no active class: uniform over all classes (cacgmm.hpp:217-226)
     f, t, m, k = 3, 260, 4, 3
