@@ -49,6 +49,10 @@ using namespace gssb;
 struct gss_b200_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // audio uploads, wave by wave, under the previous wave's kernels
+  int waves = 2;                       // GSS_B200_WAVES
+  double wave_first_frac = 0.25;       // GSS_B200_WAVE_FIRST_PCT: share of the audio in the first wave
+  long long wave_min_floats = 2 << 20; // GSS_B200_WAVE_MIN_FLOATS: no wave smaller than this (8 MB)
   std::string err;
   long long err_freq = -1;
   long long launches = 0;
@@ -261,6 +265,13 @@ struct Group {
   status_t* status = nullptr;
   int *ref = nullptr, *zeroed = nullptr;
   long long tot_audio = 0, tot_y = 0, tot_g = 0, tot_x = 0, tot_wave = 0, tot_pat = 0, tot_mask = 0;
+  // upload waves: segments [wave_first[w], wave_first[w + 1]) are copied together; the STFT and the WPE of wave w
+  // run while wave w + 1 is still on the bus (everything after the WPE runs on the whole group)
+  std::vector<int> wave_first;
+  std::vector<cudaEvent_t> wave_ev;  // audio of wave w is in HBM
+  std::vector<cudaEvent_t> marks;    // 2 per wave: after its STFT, after its WPE (stage clocks)
+  int waves_copied = 0, waves_run = 0;
+  int num_waves() const { return (int)wave_ev.size(); }
 };
 
 int pick_chunks(gss_b200_ctx* c, int T, long long ctas_one_chunk) {
@@ -443,9 +454,11 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
 }
 
 // ---- stage drivers (device side only) ---------------------------------------------
-gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
+gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first = 0, int count = -1) {
+  if (count < 0) count = g.nseg - first;
   bool any = false;
-  for (const SegDev& d : g.segs) {
+  for (int j = first; j < first + count; ++j) {
+    const SegDev& d = g.segs[j];
     if (d.wpe_active) {
       any = true;
     } else {  // pass-through (wpe.hpp:108-112)
@@ -467,8 +480,8 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
   a.fb_ticket = g.fb_ticket;
   a.fb_slots = kWpeFallbackSlots;
   a.gconj = g.gconj;
-  a.segs = g.d_segs;
-  a.status = g.status;
+  a.segs = g.d_segs + first;  // kernels index segments and their status from the launch's first one
+  a.status = g.status + first;
   a.regularization = w.regularization;
   a.M = g.M;
   a.taps = w.taps;
@@ -479,7 +492,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w) {
     CU_TRY(c, cudaMemsetAsync(g.fb_ticket, 0, sizeof(int) * kWpeFallbackSlots, c->stream));
     for (int step = 0; step < 4; ++step) {
       KClock k(c, kK_wpe_power + step);
-      CU_TRY(c, launch_wpe_step(step, a, g.nseg, g.F, g.max_T, g.max_wchunks, c->stream));
+      CU_TRY(c, launch_wpe_step(step, a, count, g.F, g.max_T, g.max_wchunks, c->stream));
     }
   }
   return GSS_OK;
@@ -607,11 +620,34 @@ namespace {
 
 void free_batch(gss_b200_ctx* c, gss_b200_batch* b) {
   if (!b) return;
-  for (auto& g : b->groups) g->mem.release();
+  for (auto& g : b->groups) {
+    // the copy stream may still be writing into the group's audio when a failed call is torn down
+    if (c && g->waves_copied > 0) cudaStreamSynchronize(c->copy_stream);
+    g->mem.release();
+    for (cudaEvent_t e : g->wave_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : g->marks) cudaEventDestroy(e);
+  }
   for (cudaEvent_t e : b->events) cudaEventDestroy(e);
   delete b;
   (void)c;
 }
+
+/// Queues the host->device copies of wave w's audio on the copy stream and marks their end.
+gss_status copy_wave(gss_b200_ctx* c, gss_b200_batch* b, Group& g, int w) {
+  for (int j = g.wave_first[w]; j < g.wave_first[w + 1]; ++j) {
+    const gss_segment_desc& d = b->desc[g.members[j]];
+    CU_TRY(c, cudaMemcpyAsync(g.audio + g.segs[j].audio_off, d.audio,
+                              sizeof(float) * (size_t)d.channels * d.num_samples, cudaMemcpyHostToDevice,
+                              c->copy_stream));
+  }
+  CU_TRY(c, cudaEventRecord(g.wave_ev[w], c->copy_stream));
+  g.waves_copied = w + 1;
+  return GSS_OK;
+}
+
+gss_status upload_impl(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs, const gss_pipeline_config* cfg,
+                       bool copy_now, gss_b200_batch** out);
+gss_status run_impl(gss_b200_ctx* c, gss_b200_batch* b);
 
 }  // namespace
 
@@ -658,6 +694,12 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
     delete c;
     return fail(nullptr, GSS_CUDA_ERROR, cudaGetErrorString(e));
   }
+  e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return fail(nullptr, GSS_CUDA_ERROR, cudaGetErrorString(e));
+  }
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     unsigned long long thr = ~0ull;  // keep freed blocks cached for the next batch
@@ -667,6 +709,10 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
   if (const char* s = std::getenv("GSS_B200_WPE_APPLY")) c->wpe_apply_tc = std::strcmp(s, "fp32") != 0;
   if (const char* s = std::getenv("GSS_B200_EM_CHUNK_FRAMES")) c->em_chunk_frames = std::atoi(s);
   if (const char* s = std::getenv("GSS_B200_WPE_CHUNK_FRAMES")) c->wpe_chunk_frames = std::atoi(s);
+  if (const char* s = std::getenv("GSS_B200_WAVES")) c->waves = std::max(1, std::atoi(s));
+  if (const char* s = std::getenv("GSS_B200_WAVE_MIN_FLOATS")) c->wave_min_floats = std::max(1LL, std::atoll(s));
+  if (const char* s = std::getenv("GSS_B200_WAVE_FIRST_PCT"))
+    c->wave_first_frac = std::min(100, std::max(1, std::atoi(s))) * 0.01;
   *out = c;
   return GSS_OK;
 }
@@ -675,6 +721,8 @@ void gss_b200_destroy(gss_b200_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  cudaStreamSynchronize(c->copy_stream);
+  cudaStreamDestroy(c->copy_stream);
   for (auto& kv : c->tables) {
     cudaFree(kv.second.tw);
     cudaFree(kv.second.win);
@@ -768,8 +816,12 @@ gss_status gss_b200_stage_ms(gss_b200_ctx* c, double* ms) {
 // ---------------------------------------------------------------------------
 // enhance_batch = upload + run + fetch
 // ---------------------------------------------------------------------------
-gss_status gss_b200_batch_upload(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
-                                 const gss_pipeline_config* cfg, gss_b200_batch** out) {
+}  // extern "C"
+
+namespace {
+
+gss_status upload_impl(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs, const gss_pipeline_config* cfg,
+                       bool copy_now, gss_b200_batch** out) {
   *out = nullptr;
   if (!c) return fail(nullptr, GSS_INTERNAL_ERROR, "null context");
   CU_TRY(c, cudaSetDevice(c->device));
@@ -852,25 +904,52 @@ gss_status gss_b200_batch_upload(gss_b200_ctx* c, int32_t n, const gss_segment_d
       free_batch(c, b);
       return rc;
     }
-    for (int j = 0; j < g->nseg; ++j) {
-      const gss_segment_desc& d = b->desc[g->members[j]];
-      cudaError_t e = cudaMemcpyAsync(g->audio + g->segs[j].audio_off, d.audio,
-                                      sizeof(float) * (size_t)d.channels * d.num_samples, cudaMemcpyHostToDevice,
-                                      c->stream);
-      if (e != cudaSuccess) {
-        g->mem.release();
-        free_batch(c, b);
-        return fail(c, GSS_CUDA_ERROR, cudaGetErrorString(e));
+    // Waves of whole segments. Only the first wave's upload is exposed, so it is small: a quarter of the audio,
+    // whose STFT + WPE (about 4x the bus time per byte on the headline shape) cover the upload of the rest.
+    // Small launches pay in tail effects, so there are two waves by default, and none below ~8 MB.
+    {
+      long long floats = 0;
+      for (int j = 0; j < g->nseg; ++j) floats += (long long)g->M * g->segs[j].N;
+      const long long min_wave = c->wave_min_floats;
+      const long long first = std::max<long long>((long long)(floats * c->wave_first_frac), min_wave);
+      const long long rest = c->waves > 1 ? std::max<long long>((floats - first) / (c->waves - 1), min_wave) : 0;
+      long long acc = 0, target = c->waves > 1 ? first : floats + 1;
+      g->wave_first.push_back(0);
+      for (int j = 0; j < g->nseg; ++j) {
+        acc += (long long)g->M * g->segs[j].N;
+        if (acc >= target && j + 1 < g->nseg && (int)g->wave_first.size() < c->waves) {
+          g->wave_first.push_back(j + 1);
+          acc = 0;
+          target = rest;
+        }
       }
+      g->wave_first.push_back(g->nseg);
+      const int nw = (int)g->wave_first.size() - 1;
+      g->wave_ev.resize(nw);
+      g->marks.resize(2 * nw);
+      for (auto& e : g->wave_ev) cudaEventCreate(&e);
+      for (auto& e : g->marks) cudaEventCreate(&e);
     }
     b->groups.push_back(std::move(g));
   }
+  // the buffers are stream-ordered allocations of the compute stream: the copy stream starts behind them (and
+  // behind whatever the compute stream was still doing with the pool's memory)
   cudaEventRecord(b->events[1], c->stream);
+  cudaStreamWaitEvent(c->copy_stream, b->events[1], 0);
+  if (copy_now)
+    for (auto& g : b->groups)
+      for (int w = 0; w < g->num_waves(); ++w) {
+        rc = copy_wave(c, b, *g, w);
+        if (rc != GSS_OK) {
+          free_batch(c, b);
+          return rc;
+        }
+      }
   *out = b;
   return GSS_OK;
 }
 
-gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) {
+gss_status run_impl(gss_b200_ctx* c, gss_b200_batch* b) {
   CU_TRY(c, cudaSetDevice(c->device));
   const gss_pipeline_config& cfg = b->cfg;
   const StftParams sp = stft_params(cfg.stft);
@@ -883,27 +962,46 @@ gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) {
     CU_TRY(c, cudaMemsetAsync(g.status, 0xFF, sizeof(status_t) * g.nseg, st));
     CU_TRY(c, cudaMemsetAsync(g.zeroed, 0, sizeof(int) * g.nseg, st));
     cudaEventRecord(ev[0], st);
-    {
-      StftArgs a;
-      a.audio = g.audio;
-      a.y = g.Y;
-      a.segs = g.d_segs;
-      a.tw_d = b->tables.tw_d;
-      a.win_d = b->tables.win_d;
-      a.p = sp;
-      a.M = g.M;
-      a.TB = 0;
-      a.fft_warps = 0;
-      KClock k(c, kK_stft);
-      CU_TRY(c, launch_stft(a, g.nseg, g.max_T, st));
+    const float2* tensor = cfg.enable_wpe ? g.Yd : g.Y;
+    if (g.waves_copied == 0) {
+      gss_status rc = copy_wave(c, b, g, 0);
+      if (rc != GSS_OK) return rc;
+    }
+    // a batch whose audio was all queued at upload time (the resident form) runs as one wave
+    const bool resident = g.waves_copied == g.num_waves();
+    g.waves_run = resident ? 1 : g.num_waves();
+    for (int w = 0; w < g.waves_run; ++w) {
+      const int first = resident ? 0 : g.wave_first[w], count = resident ? g.nseg : g.wave_first[w + 1] - first;
+      for (int v = resident ? 0 : w; v <= (resident ? g.num_waves() - 1 : w); ++v)
+        CU_TRY(c, cudaStreamWaitEvent(st, g.wave_ev[v], 0));
+      {
+        StftArgs a;
+        a.audio = g.audio;
+        a.y = g.Y;
+        a.segs = g.d_segs + first;
+        a.tw_d = b->tables.tw_d;
+        a.win_d = b->tables.win_d;
+        a.p = sp;
+        a.M = g.M;
+        a.TB = 0;
+        a.fft_warps = 0;
+        KClock k(c, kK_stft);
+        CU_TRY(c, launch_stft(a, count, g.max_T, st));
+      }
+      cudaEventRecord(g.marks[2 * w], st);
+      if (cfg.enable_wpe) {
+        gss_status rc = run_wpe(c, g, cfg.wpe, first, count);
+        if (rc != GSS_OK) return rc;
+      }
+      cudaEventRecord(g.marks[2 * w + 1], st);
+      // the next wave's audio goes on the bus behind this wave's launches: with pageable host memory the copy
+      // call blocks the host, and the device works through this wave meanwhile
+      if (!resident && w + 1 < g.num_waves() && g.waves_copied <= w + 1) {
+        gss_status rc = copy_wave(c, b, g, w + 1);
+        if (rc != GSS_OK) return rc;
+      }
     }
     cudaEventRecord(ev[1], st);
-    const float2* tensor = g.Y;
-    if (cfg.enable_wpe) {
-      gss_status rc = run_wpe(c, g, cfg.wpe);
-      if (rc != GSS_OK) return rc;
-      tensor = g.Yd;
-    }
     cudaEventRecord(ev[2], st);
     {
       EmRun r{tensor, 1, true, false, false};
@@ -955,6 +1053,17 @@ gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) {
   b->ran = true;
   return GSS_OK;
 }
+
+}  // namespace
+
+extern "C" {
+
+gss_status gss_b200_batch_upload(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
+                                 const gss_pipeline_config* cfg, gss_b200_batch** out) {
+  return upload_impl(c, n, segs, cfg, /*copy_now=*/true, out);
+}
+
+gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) { return run_impl(c, b); }
 
 gss_status gss_b200_batch_fetch(gss_b200_ctx* c, gss_b200_batch* b, gss_segment_diag* diags) {
   CU_TRY(c, cudaSetDevice(c->device));
@@ -1042,12 +1151,26 @@ gss_status gss_b200_batch_fetch(gss_b200_ctx* c, gss_b200_batch* b, gss_segment_
   // stage clocks
   for (double& v : c->stage_ms) v = 0.0;
   float ms = 0.f;
-  if (cudaEventElapsedTime(&ms, b->events[0], b->events[1]) == cudaSuccess) c->stage_ms[5] = ms;
   if (cudaEventElapsedTime(&ms, d2h0, d2h1) == cudaSuccess) c->stage_ms[6] = ms;
-  for (size_t gi = 0; gi < b->groups.size(); ++gi)
-    for (int s = 0; s < 5; ++s)
+  for (size_t gi = 0; gi < b->groups.size(); ++gi) {
+    const Group& g = *b->groups[gi];
+    // the STFT and the WPE alternate wave by wave: their stage clocks are sums over the waves (a wave's STFT
+    // clock includes any wait for its audio); the upload that is NOT hidden is what the first wave waits for
+    cudaEvent_t prev = b->events[2 + 6 * gi];
+    for (int w = 0; w < g.waves_run; ++w) {
+      if (cudaEventElapsedTime(&ms, prev, g.marks[2 * w]) == cudaSuccess) c->stage_ms[0] += ms;
+      if (cudaEventElapsedTime(&ms, g.marks[2 * w], g.marks[2 * w + 1]) == cudaSuccess) c->stage_ms[1] += ms;
+      prev = g.marks[2 * w + 1];
+    }
+    for (int s = 2; s < 5; ++s)
       if (cudaEventElapsedTime(&ms, b->events[2 + 6 * gi + s], b->events[2 + 6 * gi + s + 1]) == cudaSuccess)
         c->stage_ms[s] += ms;
+  }
+  // upload clock: from the first copy being allowed to start to the last wave being resident (most of it runs
+  // under the earlier waves' kernels)
+  if (!b->groups.empty() && !b->groups.back()->wave_ev.empty() &&
+      cudaEventElapsedTime(&ms, b->events[1], b->groups.back()->wave_ev.back()) == cudaSuccess)
+    c->stage_ms[5] = ms;
   cudaEventDestroy(d2h0);
   cudaEventDestroy(d2h1);
   // remember the first failure for gss_b200_last_error
@@ -1069,9 +1192,10 @@ void gss_b200_batch_free(gss_b200_ctx* c, gss_b200_batch* b) {
 gss_status gss_b200_enhance_batch(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
                                   const gss_pipeline_config* cfg, gss_segment_diag* diags) {
   gss_b200_batch* b = nullptr;
-  gss_status rc = gss_b200_batch_upload(c, n, segs, cfg, &b);
+  // the audio goes up wave by wave from inside the run, each wave behind the previous wave's launches
+  gss_status rc = upload_impl(c, n, segs, cfg, /*copy_now=*/false, &b);
   if (rc != GSS_OK) return rc;
-  rc = gss_b200_batch_run(c, b);
+  rc = run_impl(c, b);
   if (rc == GSS_OK) rc = gss_b200_batch_fetch(c, b, diags);
   cudaStreamSynchronize(c->stream);
   gss_b200_batch_free(c, b);

@@ -129,6 +129,28 @@ def test_resident_batch_matches_one_shot(gss):
     assert ms["mask"] > 0 and ms["stft"] > 0
 
 
+def test_upload_waves_do_not_change_the_result(gss, monkeypatch):
+    # enhance_batch uploads the audio in waves (STFT + WPE of a wave run under the next wave's copy); a segment's
+    # result does not depend on its wave, on the number of waves, or on pinned vs pageable host memory
+    from paper_2212_05271_b200 import synth
+    w = synth.workload("tiny", n_segments=5)
+    monkeypatch.setenv("GSS_B200_WAVES", "1")
+    one_wave = gss.scheduler.enhance_batches(w.segments, w.cfg, gss.Context(0))
+    monkeypatch.setenv("GSS_B200_WAVE_MIN_FLOATS", "1")  # tiny segments are far below the 8 MB wave floor
+    for waves, first_pct in ((2, 25), (3, 10), (5, 50), (9, 1)):
+        monkeypatch.setenv("GSS_B200_WAVES", str(waves))
+        monkeypatch.setenv("GSS_B200_WAVE_FIRST_PCT", str(first_pct))
+        ctx = gss.Context(0)
+        got = gss.scheduler.enhance_batches(w.segments, w.cfg, ctx)
+        rb = gss.scheduler.ResidentBatch(w.segments, w.cfg, ctx, pinned=True)
+        pinned = rb.enhance().results()
+        for a, b, c in zip(one_wave, got, pinned):
+            assert a.error is None and b.error is None and c.error is None
+            assert a.outputs[0].tobytes() == b.outputs[0].tobytes() == c.outputs[0].tobytes()
+            assert a.ll_final == b.ll_final == c.ll_final and a.ref_channel == b.ref_channel
+        assert ctx.stage_ms()["wpe"] > 0
+
+
 def oracle_unstable_bins(oracle, ss, cfg, threshold=1e-2):
     """Bins on which the ORACLE itself is unstable at the FP32 rounding level: its masks move by more than
     `threshold` (or its WPE output by more than 1e-3 relative) when its input spectrogram is multiplied by
