@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -1193,12 +1194,23 @@ gss_status gss_b200_enhance_batch(gss_b200_ctx* c, int32_t n, const gss_segment_
                                   const gss_pipeline_config* cfg, gss_segment_diag* diags) {
   gss_b200_batch* b = nullptr;
   // the audio goes up wave by wave from inside the run, each wave behind the previous wave's launches
+  static const bool trace = std::getenv("GSS_B200_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   gss_status rc = upload_impl(c, n, segs, cfg, /*copy_now=*/false, &b);
   if (rc != GSS_OK) return rc;
+  const auto t1 = std::chrono::steady_clock::now();
   rc = run_impl(c, b);
+  const auto t2 = std::chrono::steady_clock::now();
   if (rc == GSS_OK) rc = gss_b200_batch_fetch(c, b, diags);
   cudaStreamSynchronize(c->stream);
+  const auto t3 = std::chrono::steady_clock::now();
   gss_b200_batch_free(c, b);
+  if (trace) {
+    const auto t4 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[gss_b200] enhance_batch host ms: prepare %.3f, enqueue %.3f, wait+fetch %.3f, free %.3f\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+  }
   return rc;
 }
 

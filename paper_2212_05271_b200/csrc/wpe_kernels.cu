@@ -573,25 +573,45 @@ __global__ void __launch_bounds__(kSolveThreads, 4) wpe_solve2_kernel(WpeArgs a)
         if (c < pb) row[c] = x[c];
     }
     __syncthreads();
-    // 3. trailing update: A22 -= L21 L21^H (lower triangle), W2 -= W1 L21^H. Thread grid 8 x 16 over (row, col).
+    // 3. trailing update: A22 -= L21 L21^H (lower triangle), W2 -= W1 L21^H. Thread grid 8 x 16 over (row, col);
+    //    a thread takes two rows at a time so that every panel row it reads from shared memory feeds two
+    //    products (the loop is bound by those 16-byte loads, not by the FP64 pipe).
     {
       const int ty = tid >> 4, tx = tid & 15;
-      for (int t = ty; t < nbelow + M; t += 8) {
-        const bool isw = t >= nbelow;
-        cdbl* rowi = isw ? W + (t - nbelow) * km : Lp + tri(r0 + t);
-        cdbl li[kPB];
+      const int nrows = nbelow + M;
+      for (int t = ty; t < nrows; t += 16) {
+        const int t1 = t + 8;
+        const bool has1 = t1 < nrows;
+        const bool isw0 = t >= nbelow, isw1 = has1 && t1 >= nbelow;
+        cdbl* row0 = isw0 ? W + (t - nbelow) * km : Lp + tri(r0 + t);
+        cdbl* row1 = !has1 ? row0 : isw1 ? W + (t1 - nbelow) * km : Lp + tri(r0 + t1);
+        cdbl a0[kPB], a1[kPB];
 #pragma unroll
-        for (int c = 0; c < kPB; ++c) li[c] = c < pb ? rowi[kb + c] : cd_make(0.0, 0.0);
-        const int jmax = isw ? km - 1 : r0 + t;  // last column of this row to update
+        for (int c = 0; c < kPB; ++c) {
+          a0[c] = c < pb ? row0[kb + c] : cd_make(0.0, 0.0);
+          a1[c] = (has1 && c < pb) ? row1[kb + c] : cd_make(0.0, 0.0);
+        }
+        const int jmax0 = isw0 ? km - 1 : r0 + t;  // last column of each row to update
+        const int jmax1 = !has1 ? -1 : isw1 ? km - 1 : r0 + t1;
+        const int jmax = jmax0 > jmax1 ? jmax0 : jmax1;
         for (int jj = r0 + tx; jj <= jmax; jj += 16) {
           const cdbl* lj = Lp + tri(jj) + kb;
-          cdbl s0 = cd_make(0.0, 0.0), s1 = cd_make(0.0, 0.0);
+          cdbl s00 = cd_make(0.0, 0.0), s01 = s00, s10 = s00, s11 = s00;
 #pragma unroll
           for (int c = 0; c < kPB; c += 2) {
-            if (c < pb) s0 = cd_add(s0, cd_mulc(li[c], lj[c]));
-            if (c + 1 < pb) s1 = cd_add(s1, cd_mulc(li[c + 1], lj[c + 1]));
+            if (c < pb) {
+              const cdbl l = lj[c];
+              s00 = cd_add(s00, cd_mulc(a0[c], l));
+              s10 = cd_add(s10, cd_mulc(a1[c], l));
+            }
+            if (c + 1 < pb) {
+              const cdbl l = lj[c + 1];
+              s01 = cd_add(s01, cd_mulc(a0[c + 1], l));
+              s11 = cd_add(s11, cd_mulc(a1[c + 1], l));
+            }
           }
-          rowi[jj] = cd_sub(rowi[jj], cd_add(s0, s1));
+          if (jj <= jmax0) row0[jj] = cd_sub(row0[jj], cd_add(s00, s01));
+          if (jj <= jmax1) row1[jj] = cd_sub(row1[jj], cd_add(s10, s11));
         }
       }
     }
