@@ -23,7 +23,8 @@ import sys
 CLASSES = [("stft", r"^stft"), ("istft", r"^istft"), ("wpe_power", r"wpe_power"),
            ("wpe_gram", r"wpe_gram"), ("wpe_solve", r"wpe_solve"), ("wpe_apply", r"wpe_apply"),
            ("em_pass", r"em_pass"), ("em_update", r"em_update_kernel"),
-           ("mvdr", r"mvdr_|select_reference"), ("apply", r"beamform_apply"), ("other", r".")]
+           ("mvdr", r"mvdr_|select_reference"), ("apply", r"beamform_apply"), ("em_ll_sum", r"sum_ll"),
+           ("bench_fp32_peak_probe (not part of a step)", r"fma_peak"), ("other", r".")]
 
 
 def classify(name):
