@@ -9,7 +9,7 @@
 //     Re P[e][c]  = G[e][2km+c] + G[km+e][2km+M+c]     Im P[e][c]  = G[km+e][2km+c] - G[e][2km+M+c]
 // The SAME staged operand is both MMA operands (A = rows 0..127, B = all NR rows, both K-major with the
 // frame index as K), so one expansion of the slab feeds the whole product. Rows >= 128 (NR = 160 at M = 7,
-// 176 at M = 8) are covered by a second accumulator D2 = S[NR-128..NR) x S[128..NR)^T; symmetry gives the
+// 176 at M = 8) are covered by a second accumulator D2 = S[NR-64..NR) x S[128..NR)^T (M = 64); symmetry gives the
 // rest. FP32 accuracy comes from the split x = hi + lo (hi = top 19 bits): hi*hi + hi*lo + lo*hi.
 //
 // Pipeline per CTA (one (segment, bin), 256 threads): per chunk of 32 frames all warps expand the slab into
@@ -54,8 +54,8 @@ __device__ __forceinline__ uint64_t make_smem_desc(uint32_t addr, uint32_t lbo_b
 }
 
 /// kind::tf32, FP32 accumulate, both operands K-major, M = 128.
-__device__ __forceinline__ uint32_t make_idesc_tf32(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+__device__ __forceinline__ uint32_t make_idesc_tf32(int n, int m = 128) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   if (warp == kTcWorkerWarps) {
     // ===== MMA issuer =====
     if (lane == 0) {
-      const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16);
+      const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16, 64);
       for (int c = 0; c < nchunk; ++c) {
         const int b = c & 1;
         mbar_wait(&full[b], (uint32_t)((c / 2) & 1));
@@ -170,7 +170,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
           mma_tf32(d1, dh, dl, idesc1, 1u);
           mma_tf32(d1, dl, dh, idesc1, 1u);
           if (N2 > 0) {
-            const uint32_t ra = ((NR - 128) / 8) * sbo, rb = 16 * sbo;  // rows NR-128.. and rows 128..
+            // the corner is an M = 64 MMA on the last 64 rows: the kernel is bound by the operand bytes it
+            // streams from shared memory, and a 64-row A tile is half of them (row r of that accumulator
+            // lives in tensor-memory lane 32 (r / 16) + r % 16)
+            const uint32_t ra = ((NR - 64) / 8) * sbo, rb = 16 * sbo;  // rows NR-64.. and rows 128..
             const uint64_t ah = make_smem_desc(a_hi + ra + ko, lbo, sbo), al = make_smem_desc(a_lo + ra + ko, lbo, sbo);
             const uint64_t bh = make_smem_desc(a_hi + rb + ko, lbo, sbo), bl = make_smem_desc(a_lo + rb + ko, lbo, sbo);
             mma_tf32(d2, ah, bh, idesc2, accf);

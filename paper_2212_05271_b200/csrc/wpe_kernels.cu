@@ -431,7 +431,10 @@ __global__ void __launch_bounds__(kSolveThreads, 4) wpe_solve2_kernel(WpeArgs a)
   auto G = [&](int x, int y) -> double {
     if (x < 128) return (double)raw[x * NCT + y];
     if (y < 128) return (double)raw[y * NCT + x];
-    return (double)raw[(x - (NR - 128)) * NCT + NR + (y - 128)];
+    // corner accumulator (M = 64 MMA on rows NR-64..NR): row r sits in tensor-memory lane 32 (r / 16) + r % 16,
+    // and the Gram kernel writes lane l to row l of `raw`
+    const int r = x - (NR - 64);
+    return (double)raw[((r >> 4) * 32 + (r & 15)) * NCT + NR + (y - 128)];
   };
   auto load_r = [&](int i, int j) -> cdbl {
     double re, im;
