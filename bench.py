@@ -130,11 +130,13 @@ def algorithmic_work(segs, cfg):
             w["wpe_apply"]["flops"] += J * FT * 8 * km * M
             w["wpe_apply"]["bytes"] += J * 2 * 8 * FT * M
         if J:
-            # tensor-core Gram: executed TF32 flops (3xTF32 split, padded 128 x (NR + N2) real accumulator)
+            # tensor-core Gram: executed TF32 flops (3xTF32 split; a 128 x NR accumulator plus the corner block as
+            # an M = 64 MMA of N2 columns; the tensor core's cost floor is that of M = 128 for either)
             kmp = (km + 7) // 8 * 8
             nr = (2 * kmp + 16 + 15) // 16 * 16
-            nct = nr + max(0, nr - 128)
-            w["wpe_gram"]["tensor_flops"] = w["wpe_gram"].get("tensor_flops", 0.0) + J * FT * 3 * 2 * 128 * nct
+            n2 = max(0, nr - 128)
+            w["wpe_gram"]["tensor_flops"] = (w["wpe_gram"].get("tensor_flops", 0.0) +
+                                             J * FT * 3 * 2 * (128 * nr + 64 * n2))
             # tensor-core prediction: per frame and tap 2 k-steps of 8, A_hi x [B_hi | B_lo] (N = 32) + A_lo x B_hi (N = 16)
             w["wpe_apply"]["tensor_flops"] = w["wpe_apply"].get("tensor_flops", 0.0) + J * FT * cfg.wpe.taps * 2 * 2 * 8 * 48
         w["em_pass"]["flops"] += (I + 1) * FT * (3 * M * M + 4 * M * M * K + 20 * K)

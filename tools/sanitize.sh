@@ -1,0 +1,8 @@
+#!/bin/bash
+# compute-sanitizer over the smoke path (tiny workload: every kernel class once). usage (under gpurun): bash tools/sanitize.sh <tag>
+tag=${1:-r01}
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python __graft_entry__.py smoke > gpurun_out/sanitizer_${tool}_$tag.log 2>&1
+  echo "== $tool: exit $?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|smoke:" gpurun_out/sanitizer_${tool}_$tag.log | tail -4
+done
