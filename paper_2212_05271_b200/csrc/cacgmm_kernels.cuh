@@ -314,7 +314,11 @@ __global__ void __launch_bounds__(KT * 32) em_update_kernel(EmUpdateArgs a) {
   __shared__ double s_pi[KT], s_ld[KT];
 
   const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef GSS_EXP_UPD_REVERSE
+  const int f = (int)gridDim.x - 1 - (int)blockIdx.x, seg = blockIdx.y;
+#else
   const int f = blockIdx.x, seg = blockIdx.y;
+#endif
   const SegDev sd = a.segs[seg];
   const bool live = k < sd.K;
   const long long fk = sd.fk_off + (long long)f * KT + k;

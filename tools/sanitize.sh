@@ -6,3 +6,8 @@ for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python __graft_entry__.py smoke > gpurun_out/sanitizer_${tool}_$tag.log 2>&1
   echo "== $tool: exit $?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|smoke:" gpurun_out/sanitizer_${tool}_$tag.log | tail -4
 done
+# the headline shape (7 channels, 3 speakers + noise, WPE, 40 s window): the tcgen05 kernels and the M = 7, K = 4 sweep
+for tool in memcheck racecheck; do
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python tools/parity_probe.py cfg2 > gpurun_out/sanitizer_${tool}_cfg2_$tag.log 2>&1
+  echo "== $tool cfg2: exit $?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|SDR" gpurun_out/sanitizer_${tool}_cfg2_$tag.log | tail -4
+done
