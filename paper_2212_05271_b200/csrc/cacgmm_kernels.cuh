@@ -303,8 +303,12 @@ __device__ __noinline__ bool warp_eig_floor_inverse(const cdbl* b, cdbl* a, cdbl
   return true;
 }
 
+/// Blocks per SM the update is compiled for: about 20 warps (the kernel is FP64 latency chains, more resident
+/// warps hide them; measured on cfg2, KT = 4: 2.07 ms per step at 3 blocks, 1.77 at 4, 1.72 at 5 - 6, 1.87 at 8).
+constexpr int em_update_min_blocks(int KT) { return 20 / KT < 2 ? 2 : 20 / KT > 8 ? 8 : 20 / KT; }
+
 template <int M, int L, int KT>
-__global__ void __launch_bounds__(KT * 32) em_update_kernel(EmUpdateArgs a) {
+__global__ void __launch_bounds__(KT * 32, em_update_min_blocks(KT)) em_update_kernel(EmUpdateArgs a) {
   using Lay = EmLayout<M, L>;
   using PL = PartLayout<M, L, KT, KT>;
   constexpr int NDOF = Lay::NDOF;
