@@ -221,15 +221,18 @@ __device__ __noinline__ bool warp_eig_floor_inverse(const cdbl* b, cdbl* a, cdbl
         bool act = q < M;
         if (act) {
           const cdbl apq = a[p * M + q];
-          const double mag = sqrt(cd_norm(apq));
-          if (mag == 0.0) {
+          const double n2 = cd_norm(apq);
+          if (n2 == 0.0) {
             act = false;
           } else {
+            // one reciprocal square root serves the phase and tau, another the cosine: the rotation is a chain of
+            // dependent FP64 special functions on four lanes while the other 28 wait for it
             const double app = a[p * M + p].re, aqq = a[q * M + q].re;
-            const cdbl ph = cd_make(apq.re / mag, apq.im / mag);  // e^{i phi}
-            const double tau = (aqq - app) / (2.0 * mag);
+            const double inv_mag = rsqrt(n2);
+            const cdbl ph = cd_make(apq.re * inv_mag, apq.im * inv_mag);  // e^{i phi}
+            const double tau = 0.5 * (aqq - app) * inv_mag;
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            const double c = 1.0 / sqrt(1.0 + t * t), sn = t * c;
+            const double c = rsqrt(1.0 + t * t), sn = t * c;
             // J columns: p -> [c ; -s e^{-i phi}], q -> [s ; c e^{-i phi}]
             jpp = cd_make(c, 0.0);
             jqp = cd_make(-sn * ph.re, sn * ph.im);
