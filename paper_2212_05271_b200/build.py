@@ -10,6 +10,7 @@ from __future__ import annotations
 import argparse
 import concurrent.futures as cf
 import os
+import tempfile
 import subprocess
 import sys
 
@@ -58,7 +59,10 @@ def build_variant(tag: str, flags: list[str], jobs: int | None = None) -> str:
     global OBJ, LIB, EXTRA_FLAGS
     saved = (OBJ, LIB, EXTRA_FLAGS)
     try:
-        OBJ, LIB, EXTRA_FLAGS = os.path.join(HERE, "build", "variant_" + tag), os.path.join(LIB_DIR, f"libgss_b200_{tag}.so"), list(flags)
+        # objects of an experiment go to the system scratch directory: they would otherwise travel with every
+        # gpurun snapshot (only the library has to)
+        obj = os.path.join(tempfile.gettempdir(), "gss_b200_variant_" + tag)
+        OBJ, LIB, EXTRA_FLAGS = obj, os.path.join(LIB_DIR, f"libgss_b200_{tag}.so"), list(flags)
         return build(False, jobs)
     finally:
         OBJ, LIB, EXTRA_FLAGS = saved
