@@ -149,6 +149,18 @@ def test_upload_waves_do_not_change_the_result(gss, monkeypatch):
             assert a.outputs[0].tobytes() == b.outputs[0].tobytes() == c.outputs[0].tobytes()
             assert a.ll_final == b.ll_final == c.ll_final and a.ref_channel == b.ref_channel
         assert ctx.stage_ms()["wpe"] > 0
+    # several shape groups in one call, each with its own waves (the copy stream is shared)
+    from paper_2212_05271_b200.gss import scheduler, stft, wpe
+    cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(6, 2, 2, 0, 1e-10), True, 4)
+    mixed = [synth.make_supersegment(910 + i, m, k, 1.5, 0.5, cfg)
+             for i, (m, k) in enumerate([(4, 2), (7, 3), (4, 2), (2, 2), (7, 3), (4, 2), (7, 3)])]
+    monkeypatch.setenv("GSS_B200_WAVES", "1")
+    want = gss.scheduler.enhance_batches(mixed, cfg, gss.Context(0))
+    monkeypatch.setenv("GSS_B200_WAVES", "3")
+    monkeypatch.setenv("GSS_B200_WAVE_FIRST_PCT", "30")
+    got = gss.scheduler.enhance_batches(mixed, cfg, gss.Context(0))
+    for a, b in zip(want, got):
+        assert a.error is None and b.error is None and a.outputs[0].tobytes() == b.outputs[0].tobytes()
 
 
 def oracle_unstable_bins(oracle, ss, cfg, threshold=1e-2):
