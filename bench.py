@@ -123,7 +123,9 @@ def algorithmic_work(segs, cfg):
         w["stft"]["bytes"] += 4 * M * N + 8 * FT * M
         w["stft"]["flops"] += M * T * (2.5 * n * math.log2(n) + n)
         if J:
-            w["wpe_power"]["bytes"] += J * (8 * FT * M + 4 * FT)
+            # with psd_context 0 the tensor-core prediction writes the next iteration's weights: one power pass
+            n_power = 1 if (cfg.wpe.psd_context == 0 and os.environ.get("GSS_B200_WPE_APPLY") != "fp32") else J
+            w["wpe_power"]["bytes"] += n_power * (8 * FT * M + 4 * FT)
             w["wpe_gram"]["flops"] += J * FT * 8 * (km * (km + 1) / 2 + km * M)
             w["wpe_gram"]["bytes"] += J * (8 * FT * M + 4 * FT)
             w["wpe_solve"]["flops"] += J * F * (8 / 3 * km ** 3 + 16 * km * km * M)

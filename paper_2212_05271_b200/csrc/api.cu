@@ -477,6 +477,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first
   a.use_tc = g.use_tc;
   a.apply_tc = c->wpe_apply_tc && wpe_apply_tc_supported(w.taps, w.delay, g.M);
   a.debug_rp = nullptr;
+  a.w_next = nullptr;
   a.fb_scratch = g.fb_scratch;
   a.fb_ticket = g.fb_ticket;
   a.fb_slots = kWpeFallbackSlots;
@@ -488,13 +489,20 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first
   a.taps = w.taps;
   a.delay = w.delay;
   a.psd_context = w.psd_context;
+  // With psd_context 0 the next iteration's weights are the power of the frames the prediction kernel has just
+  // written: the tensor-core kernel emits them and the power pass runs for the first iteration only.
+  const bool fuse_power = a.apply_tc && w.psd_context == 0;
+  bool w_ready = false;
   for (int it = 0; it < w.iterations; ++it) {
     a.ycur = it == 0 ? g.Y : g.Yd;
+    a.w_next = fuse_power && it + 1 < w.iterations ? g.w : nullptr;
     CU_TRY(c, cudaMemsetAsync(g.fb_ticket, 0, sizeof(int) * kWpeFallbackSlots, c->stream));
     for (int step = 0; step < 4; ++step) {
+      if (step == 0 && w_ready) continue;
       KClock k(c, kK_wpe_power + step);
       CU_TRY(c, launch_wpe_step(step, a, count, g.F, g.max_T, g.max_wchunks, c->stream));
     }
+    w_ready = a.w_next != nullptr;
   }
   return GSS_OK;
 }
@@ -1422,6 +1430,7 @@ gss_status gss_b200_debug_wpe_gram(gss_b200_ctx* c, const float* in, int32_t bin
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
   a.apply_tc = 0;
+  a.w_next = nullptr;
   a.debug_rp = d_rp;
   a.fb_scratch = g.fb_scratch;
   a.fb_ticket = g.fb_ticket;

@@ -55,6 +55,7 @@ struct WpeArgs {
   cdbl* debug_rp;       // non-null: the solve kernel only dumps hermitized R (km x km) and P (km x M) per bin
   int use_tc;           // 1: the Gram of this iteration came from wpe_gram_tc_kernel
   int apply_tc;         // 1: the prediction runs on the tensor cores (wpe_apply_tc_kernel)
+  float* w_next;        // tensor-core prediction only: also write the NEXT iteration's Gram weights (psd_context 0)
 };
 /// cdbl elements of one scratch slot of the WPE solve's eigenvalue-floor fallback: A, two work matrices, B, eigenvalues
 __host__ __device__ inline int wpe_fallback_slot_elems(int km, int M) { return 3 * km * km + km * M + km / 2 + 1; }

@@ -248,10 +248,21 @@ __global__ void __launch_bounds__(kAppThreads) wpe_apply_tc_kernel(WpeArgs a) {
           o[4 * kc + 2] = h4.z + l4.z;
           o[4 * kc + 3] = h4.w + l4.w;
         }
+        float pw = 0.f;  // squared norm of the output frame, accumulated like wpe_power_kernel does
 #pragma unroll
-        for (int c = 0; c < M; ++c)
-          of[(long long)t * M + c] =
-              make_float2(o[2 * c] - __uint_as_float(r[c]), o[2 * c + 1] - __uint_as_float(r[8 + c]));
+        for (int c = 0; c < M; ++c) {
+          const float2 v = make_float2(o[2 * c] - __uint_as_float(r[c]), o[2 * c + 1] - __uint_as_float(r[8 + c]));
+          of[(long long)t * M + c] = v;
+          pw += v.x * v.x + v.y * v.y;
+        }
+        // the next iteration's lambda_t is the power of exactly this frame (wpe.hpp:40-56 with psd_context 0):
+        // writing 1 / lambda here saves that iteration's pass over the tensor
+        if (a.w_next != nullptr) {
+          // (double)pw / M rounded to float: the reciprocal multiply differs from the division by at most one
+          // ulp of a double, which the rounding to float absorbs
+          const float lambda = fmaxf((float)kPowerFloor, (float)((double)pw * (1.0 / (double)M)));
+          a.w_next[sd.w_off + (long long)f * sd.T + t] = __frcp_rn(lambda);
+        }
       }
     };
 
