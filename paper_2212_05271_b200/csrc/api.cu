@@ -105,6 +105,21 @@ struct KClock {
     if (b) cudaEventRecord(b, c->stream);
   }
 };
+/// A pair of timing events destroyed on every exit path.
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaError_t create() {
+    cudaError_t e = cudaEventCreate(&a);
+    return e != cudaSuccess ? e : cudaEventCreate(&b);
+  }
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  EventPair() = default;
+  EventPair(const EventPair&) = delete;
+  EventPair& operator=(const EventPair&) = delete;
+};
 constexpr int kWpeFallbackSlots = 32;  // concurrent eigenvalue-floor repairs per WPE launch; further bins wait for a slot
 enum KernelId { kK_stft = 0, kK_wpe_power, kK_wpe_gram, kK_wpe_solve, kK_wpe_apply, kK_em_pass, kK_em_update,
                 kK_mvdr, kK_apply, kK_istft, kK_misc };
@@ -633,10 +648,13 @@ void free_batch(gss_b200_ctx* c, gss_b200_batch* b) {
     // the copy stream may still be writing into the group's audio when a failed call is torn down
     if (c && g->waves_copied > 0) cudaStreamSynchronize(c->copy_stream);
     g->mem.release();
-    for (cudaEvent_t e : g->wave_ev) cudaEventDestroy(e);
-    for (cudaEvent_t e : g->marks) cudaEventDestroy(e);
+    for (cudaEvent_t e : g->wave_ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : g->marks)
+      if (e) cudaEventDestroy(e);
   }
-  for (cudaEvent_t e : b->events) cudaEventDestroy(e);
+  for (cudaEvent_t e : b->events)
+    if (e) cudaEventDestroy(e);
   delete b;
   (void)c;
 }
@@ -796,9 +814,9 @@ gss_status gss_b200_fp32_peak(gss_b200_ctx* c, double* tflops) {
   cudaDeviceProp prop;
   CU_TRY(c, cudaGetDeviceProperties(&prop, c->device));
   const int ctas = prop.multiProcessorCount * 8, iters = 2048;
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
+  EventPair ev;
+  CU_TRY(c, ev.create());
+  cudaEvent_t a = ev.a, b = ev.b;
   double best = 0.0;
   for (int rep = 0; rep < 6; ++rep) {
     cudaEventRecord(a, c->stream);
@@ -810,8 +828,6 @@ gss_status gss_b200_fp32_peak(gss_b200_ctx* c, double* tflops) {
     if (e == cudaSuccess && rep > 0 && ms > 0.f)
       best = std::max(best, 2.0 * 256.0 * iters * 256.0 * ctas / (ms * 1e-3) * 1e-12);
   }
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
   cudaFree(scratch);
   *tflops = best;
   return GSS_OK;
@@ -897,8 +913,12 @@ gss_status upload_impl(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
     s.index = i;
     by_shape[std::make_pair(d.channels, em_class_tier(d.num_classes))].push_back(s);
   }
-  b->events.resize(2 + 6 * by_shape.size());
-  for (auto& e : b->events) cudaEventCreate(&e);
+  b->events.assign(2 + 6 * by_shape.size(), nullptr);
+  for (auto& e : b->events)
+    if (cudaError_t ce = cudaEventCreate(&e); ce != cudaSuccess) {
+      free_batch(c, b);
+      return fail(c, GSS_CUDA_ERROR, std::string("cudaEventCreate: ") + cudaGetErrorString(ce));
+    }
   cudaEventRecord(b->events[0], c->stream);
   Needs need;
   need.audio = need.y = need.x = need.wave = need.em = need.mvdr = true;
@@ -934,10 +954,18 @@ gss_status upload_impl(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
       }
       g->wave_first.push_back(g->nseg);
       const int nw = (int)g->wave_first.size() - 1;
-      g->wave_ev.resize(nw);
-      g->marks.resize(2 * nw);
-      for (auto& e : g->wave_ev) cudaEventCreate(&e);
-      for (auto& e : g->marks) cudaEventCreate(&e);
+      g->wave_ev.assign(nw, nullptr);
+      g->marks.assign(2 * nw, nullptr);
+      cudaError_t ce = cudaSuccess;
+      for (auto& e : g->wave_ev)
+        if (ce == cudaSuccess) ce = cudaEventCreate(&e);
+      for (auto& e : g->marks)
+        if (ce == cudaSuccess) ce = cudaEventCreate(&e);
+      if (ce != cudaSuccess) {
+        b->groups.push_back(std::move(g));  // free_batch destroys what was created
+        free_batch(c, b);
+        return fail(c, GSS_CUDA_ERROR, std::string("cudaEventCreate: ") + cudaGetErrorString(ce));
+      }
     }
     b->groups.push_back(std::move(g));
   }
@@ -1089,9 +1117,9 @@ gss_status gss_b200_batch_fetch(gss_b200_ctx* c, gss_b200_batch* b, gss_segment_
     diags[i].ll_final = 0.0;
     for (int p = 0; p < b->desc[i].num_parts; ++p) b->desc[i].out_lengths[p] = 0;
   }
-  cudaEvent_t d2h0, d2h1;
-  cudaEventCreate(&d2h0);
-  cudaEventCreate(&d2h1);
+  EventPair d2h;
+  CU_TRY(c, d2h.create());
+  cudaEvent_t d2h0 = d2h.a, d2h1 = d2h.b;
   cudaEventRecord(d2h0, st);
   // small per-segment results first (they decide which waveforms are copied)
   struct Small {
@@ -1180,8 +1208,6 @@ gss_status gss_b200_batch_fetch(gss_b200_ctx* c, gss_b200_batch* b, gss_segment_
   if (!b->groups.empty() && !b->groups.back()->wave_ev.empty() &&
       cudaEventElapsedTime(&ms, b->events[1], b->groups.back()->wave_ev.back()) == cudaSuccess)
     c->stage_ms[5] = ms;
-  cudaEventDestroy(d2h0);
-  cudaEventDestroy(d2h1);
   // remember the first failure for gss_b200_last_error
   for (int i = 0; i < b->n; ++i)
     if (b->fails[i].code != GSS_OK) {

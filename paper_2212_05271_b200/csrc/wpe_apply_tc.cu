@@ -299,7 +299,9 @@ __global__ void __launch_bounds__(kAppThreads) wpe_apply_tc_kernel(WpeArgs a) {
 int wpe_apply_tc_supported(int taps, int delay, int M) {
   const int H = delay + taps - 1;
   const size_t smem = 128 + sizeof(float) * (2 * (size_t)taps * 256 + 4 * (size_t)(4 * app_rows(H) * 4));
-  return M >= 1 && M <= 8 && smem <= 100 * 1024 ? 1 : 0;
+  // a tile stages row w and, when there are more than kTile rows, row kTile + w: at most 2 * kTile slab rows, so the
+  // history H = delay + taps - 1 has to fit the second half (larger H runs the FP32 kernel wpe_apply2_kernel)
+  return M >= 1 && M <= 8 && app_rows(H) <= 2 * kTile && smem <= 100 * 1024 ? 1 : 0;
 }
 
 template <int M>

@@ -169,7 +169,11 @@ def assemble_indices(parts_start_dur, sample_rate: int, rec_samples: int, contex
     spans = np.zeros(2 * (n + 2), dtype=np.int64)
     pb = np.zeros(max(n, 1), dtype=np.int64)
     pe = np.zeros(max(n, 1), dtype=np.int64)
-    cap = int(rec_samples // max(stft.shift, 1) + 2 + 2 * n)
+    # spans are concatenated, so overlapping parts of one speaker make the assembled signal longer than the
+    # recording: size the frame-centre buffer from the span total (each span within a sample of llround(dur * sr))
+    sr = float(sample_rate)
+    total_cap = int(sum(llround(max(d, 0.0) * sr) + 1 for d in durs)) + 2 * (llround(max(context_duration, 0.0) * sr) + 1)
+    cap = int(total_cap // max(stft.shift, 1) + 2 + 2 * n)
     centers = np.zeros(cap, dtype=np.int64)
     nsp, total, nc = C.c_int32(), C.c_int64(), C.c_int64()
     cl, cr = C.c_double(), C.c_double()
@@ -283,8 +287,10 @@ class _Marshalled:
             for ln in self.out_len[i][: self.desc[i].num_parts]:
                 outs.append(np.array(self.out_wave[i][off: off + int(ln)], copy=True))
                 off += int(ln)
+            # mono may live in pinned memory owned by this object: hand out a copy, never a view
+            mono = None if self.mono[i] is None else np.array(self.mono[i], copy=True)
             res.append(EnhancementResult(outs, float(dg.ll_final), int(dg.zeroed_bins), int(dg.ref_channel),
-                                         int(dg.frames), None, self.mono[i], self.gamma[i], self.h[i]))
+                                         int(dg.frames), None, mono, self.gamma[i], self.h[i]))
         return res
 
 
@@ -369,11 +375,22 @@ class OrderedBatchQueue:
         self.cv = threading.Condition()
         self.ready = {}
         self.next = 0
+        self.closed = False
 
-    def put(self, item: LoadedBatch) -> None:
+    def put(self, item: LoadedBatch) -> bool:
+        """False when the queue was closed (the consumer is gone): the loader should stop."""
         with self.cv:
-            self.cv.wait_for(lambda: item.index < self.next + self.capacity)
+            self.cv.wait_for(lambda: self.closed or item.index < self.next + self.capacity)
+            if self.closed:
+                return False
             self.ready[item.index] = item
+            self.cv.notify_all()
+            return True
+
+    def close(self) -> None:
+        """Releases every loader blocked in put(); used when the consumer leaves abnormally."""
+        with self.cv:
+            self.closed = True
             self.cv.notify_all()
 
     def take(self) -> LoadedBatch:
@@ -515,10 +532,17 @@ def run_pipeline(recordings, segments, cfg: PipelineConfig, devices=None, gpu_ba
     def drain(limit):
         while len(inflight) > limit:
             items, fut = inflight.pop(0)
-            results = iter(fut.result()) if fut is not None else iter(())
+            try:
+                results = iter(fut.result()) if fut is not None else iter(())
+            except Exception as exc:  # call-level device failure: its batches fail, the run goes on
+                for it in items:
+                    st["load"] += it.load_seconds
+                    fail_batch(it.index, it.error if it.batch is None else "%s: %s" % (type(exc).__name__, exc))
+                continue
             for it in items:
                 consume(it, next(results) if it.batch is not None else None)
 
+    queue = None
     try:
         if cfg.workers == 0:
             source = (load_one(i) for i in range(len(plans)))
@@ -534,7 +558,8 @@ def run_pipeline(recordings, segments, cfg: PipelineConfig, devices=None, gpu_ba
                         i = next(ticket, None)
                     if i is None:
                         return
-                    queue.put(load_one(i))
+                    if not queue.put(load_one(i)):
+                        return
 
             loaders = [threading.Thread(target=loader, name="gss-loader%d" % w) for w in range(cfg.workers)]
             for t in loaders:
@@ -556,6 +581,8 @@ def run_pipeline(recordings, segments, cfg: PipelineConfig, devices=None, gpu_ba
         for t in loaders:
             t.join()
     finally:
+        if queue is not None:
+            queue.close()  # a no-op after a normal run; on an exception it lets blocked loaders leave
         if writer:
             with write_cv:
                 write_state["done"] = True

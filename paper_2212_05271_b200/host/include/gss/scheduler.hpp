@@ -311,7 +311,11 @@ inline SuperSegment assemble(const BatchPlan& plan, const manifests::Recording& 
     durs.push_back(seg.duration);
   }
   std::vector<int64_t> spans(2 * (n + 2)), pb(n), pe(n);
-  const int64_t cap = rec_samples / std::max(cfg.stft.shift, 1) + 2 + 2 * static_cast<int64_t>(n);
+  // spans are concatenated: overlapping parts make the assembled signal longer than the recording, so the
+  // frame-centre buffer is sized from the span total (each span is within a sample of llround(duration * sr))
+  int64_t total_cap = 2 * (std::llround(std::max(cfg.context_duration, 0.0) * sr) + 1);
+  for (double d : durs) total_cap += std::llround(std::max(d, 0.0) * sr) + 1;
+  const int64_t cap = total_cap / std::max(cfg.stft.shift, 1) + 2 + 2 * static_cast<int64_t>(n);
   std::vector<int64_t> centers(static_cast<size_t>(cap));
   int32_t n_spans = 0;
   int64_t total = 0, n_centers = 0;

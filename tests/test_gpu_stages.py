@@ -137,6 +137,24 @@ def test_wpe_matches_oracle(gss, oracle, f, t, m, taps, delay, iters, ctx):
     assert again.tobytes() == got.tobytes()
 
 
+@pytest.mark.parametrize("m,taps,delay", [(3, 10, 120), (7, 10, 119), (4, 4, 130), (8, 3, 126)])
+def test_wpe_long_prediction_delay(gss, oracle, m, taps, delay):
+    # history H = delay + taps - 1 around the 128 slab rows the tensor-core prediction can stage beside a tile:
+    # H <= 128 stays on tcgen05, H > 128 must take the FP32 kernel (it once read unstaged shared memory)
+    rng = np.random.RandomState(m * 1000 + delay)
+    f, t = 3, 900
+    s = (rng.randn(f, t, m) + 1j * rng.randn(f, t, m)).astype(np.complex64)
+    y = s.copy()
+    y[:, delay:, :] += 0.6 * s[:, :-delay, :]
+    y[:, delay + 2:, :] += 0.3 * np.roll(s, 1, axis=2)[:, :-(delay + 2), :]
+    cfg = gss.wpe.WpeConfig(taps, delay, 2, 0, 1e-10)
+    got = gss.wpe.dereverberate(spec(gss, y), cfg).data
+    want = oracle.wpe(y, oracle.wpe_cfg(taps, delay, 2, 0, 1e-10))
+    assert rel_fro(got, want) < 1e-4, rel_fro(got, want)
+    # the echo is predictable from the delayed taps: the output must be closer to the dry signal than the input
+    assert np.linalg.norm(got - s) < 0.7 * np.linalg.norm(y - s)
+
+
 def test_wpe_eigen_floor_fallback(gss, oracle):
     # numerics.hpp:58-73, 90-93 through the WPE solve: a silent channel and regularization 0 make R exactly
     # singular, the Cholesky pivot is 0, and the solve must fall back to the eigenvalue floor like the oracle

@@ -103,6 +103,29 @@ def test_assemble_clips_context_at_the_recording_edges(tmp_path):  # test_schedu
     assert b.context_left == pytest.approx(1.0) and b.context_right == pytest.approx(0.0)
 
 
+def test_assemble_overlapping_parts_are_longer_than_the_recording(tmp_path):
+    # scheduler.hpp:196-222: spans are concatenated as they come, so overlapping parts of one speaker are
+    # assembled twice and the right context starts at the LAST part's end (not the furthest end)
+    st = stft.StftConfig()
+    ap = sc.assemble_indices([(0.0, 40.0), (1.0, 1.0)], 16000, 41 * 16000, 15.0, st)
+    sr = 16000
+    assert ap.spans == [(0, 40 * sr), (1 * sr, 2 * sr), (2 * sr, 17 * sr)]
+    assert ap.total == 56 * sr and len(ap.frame_centers) == stft.frame_count(56 * sr, st)
+    assert list(ap.part_begin) == [0, 40 * sr] and list(ap.part_end) == [40 * sr, 41 * sr]
+    assert ap.context_left == 0.0 and ap.context_right == 15.0
+    # centres walk the spans in source time: the second span starts again at 1 s
+    t = (40 * sr + st.shift - 1) // st.shift
+    assert ap.frame_centers[t] == 1 * sr + (t * st.shift - 40 * sr)
+    assert ap.frame_centers[-1] == 17 * sr - 1
+    # the whole loader path
+    rec, src = write_recording(tmp_path, "rec", 5.0, 1, 21)
+    segs = [seg("a", "rec", "s", 0.5, 3.0), seg("b", "rec", "s", 1.0, 1.0)]
+    ss = sc.assemble(sc.BatchPlan("rec", "s", segs), rec, segs, fast_config(str(tmp_path)))
+    h = sr // 2
+    want = np.concatenate([src[:, 0:h], src[:, h:7 * h], src[:, 2 * h:4 * h], src[:, 4 * h:6 * h]], axis=1)
+    assert ss.audio.num_samples() == 11 * h > rec.num_samples() - 1 and ss.audio.channels.tobytes() == want.tobytes()
+
+
 def test_assemble_rejects_empty_sample_ranges_and_honors_channel_subsets(tmp_path):
     rec, src = write_recording(tmp_path, "rec", 2.0, 3, 8)
     cfg = fast_config(str(tmp_path))
@@ -137,3 +160,36 @@ def test_ordered_queue_hands_out_plan_order():  # scheduler.hpp:383-412
         t.join()
     consumer.join()
     assert got == [0, 1, 2, 3]
+
+
+def test_ordered_queue_close_releases_blocked_loaders():
+    import threading
+    q = sc.OrderedBatchQueue(1)
+    done = []
+    t = threading.Thread(target=lambda: done.append(q.put(sc.LoadedBatch(5))))  # far ahead of the window: blocks
+    t.start()
+    t.join(0.1)
+    assert t.is_alive()
+    q.close()
+    t.join(5)
+    assert not t.is_alive() and done == [False]
+
+
+@pytest.mark.parametrize("workers", [0, 3])
+def test_run_pipeline_turns_a_device_failure_into_batch_failures(tmp_path, workers):
+    # A call-level failure of the compute slot (here: a device that does not exist, on any box) must fail that
+    # slot's batches and let the run finish with a summary, as the C++ mirror does, instead of escaping from
+    # run_pipeline with the loader threads still blocked in the queue.
+    import json
+    import threading
+    rec, _ = write_recording(tmp_path, "rec", 6.0, 2, 4)
+    segs = [seg("s-%d" % i, "rec", "s", 0.5 + i, 0.8) for i in range(5)]
+    cfg = fast_config(str(tmp_path / "out"))
+    cfg.workers, cfg.queue_capacity, cfg.mode = workers, 1, sc.ONE_PER_BATCH
+    before = threading.active_count()
+    run = sc.run_pipeline([rec], segs, cfg, devices=[999], gpu_batch=2)
+    assert run.failed_segments == 5 and run.json["segments_written"] == 0
+    assert sorted(f["segment_id"] for f in run.json["failures"]) == [s.id for s in segs]
+    assert all("Error" in f["error"] for f in run.json["failures"])
+    assert json.load(open(cfg.out_dir + "/summary.json"))["failures"] == run.json["failures"]
+    assert threading.active_count() == before  # loaders, writer and slot threads are gone
