@@ -154,7 +154,8 @@ def algorithmic_work(segs, cfg):
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
-    from paper_2212_05271_b200 import gss, synth
+    from paper_2212_05271_b200 import gss
+    import synthbench as synth
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -345,7 +346,7 @@ def cpu_baseline(wl, n_sample=8):
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     wl = synth.workload(args.workload, n_segments=1)
     orc = load_oracle()
     cfg = wl.cfg

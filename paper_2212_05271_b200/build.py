@@ -19,8 +19,6 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libgss_b200.so")
-SYNTH_SRC = os.path.join(HERE, "synth", "gss_synth.cpp")
-SYNTH_LIB = os.path.join(HERE, "synth", "libgss_synth.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -90,8 +88,6 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = True) ->
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
-    if _mtime(SYNTH_LIB) < _mtime(SYNTH_SRC):
-        subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", SYNTH_LIB, SYNTH_SRC], check=True)
     return LIB
 
 

@@ -1,11 +1,14 @@
 """Synthetic multi-speaker reverberant mixtures and the BASELINE.json workloads (bench / test harness).
 
-`generate` binds synth/gss_synth.cpp, a restatement of the input specification of the reference's
-synthbench::generate (synthbench.hpp:323-438). Not part of the enhancement product path.
+`generate` binds synthbench/gss_synth.cpp, a restatement of the input specification of the reference's
+synthbench::generate (synthbench.hpp:323-438). Harness code (bench / tests / the ablation CLI): it lives outside
+the product package, and the enhancement path never imports it. The SI-SDR metrics, oracle-mask MVDR, canned
+fixtures and the ablation grid of synthbench.hpp:448-726 / cli.hpp:228-318 are in synthbench/harness.py.
 """
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from concurrent.futures import ThreadPoolExecutor
@@ -13,7 +16,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ..gss import manifests, scheduler, stft, wpe
+from paper_2212_05271_b200.capi import SpecError
+from paper_2212_05271_b200.gss import manifests, scheduler, stft, wpe
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "libgss_synth.so")
@@ -32,8 +36,10 @@ def _load():
 
 
 def generate(duration: float, sample_rate: int, channels: int, seed: int, speakers, reverb_t60: float = 0.3,
-             noise_snr: float = 20.0) -> np.ndarray:
-    """speakers: list (one entry per speaker) of lists of (start, duration) seconds. Returns (M, N) float32."""
+             noise_snr: float = 20.0, with_sources: bool = False):
+    """speakers: list (one entry per speaker) of lists of (start, duration) seconds. Returns the (M, N) float32
+    mixture; with `with_sources` also the per-speaker dry tracks and channel-0 images, both (K, N)
+    (GeneratedMixture::dry / images0, synthbench.hpp:166-172)."""
     lib = _load()
     offs = [0]
     starts, durs = [], []
@@ -42,8 +48,10 @@ def generate(duration: float, sample_rate: int, channels: int, seed: int, speake
             starts.append(float(s))
             durs.append(float(d))
         offs.append(len(starts))
-    n = int(round(duration * sample_rate))
+    n = int(math.floor(duration * sample_rate + 0.5))
     mix = np.zeros((channels, n), dtype=np.float32)
+    dry = np.zeros((len(speakers), n), dtype=np.float32) if with_sources else None
+    img = np.zeros((len(speakers), n), dtype=np.float32) if with_sources else None
     offs_a = np.array(offs, dtype=np.int32)
     st = np.array(starts, dtype=np.float64)
     du = np.array(durs, dtype=np.float64)
@@ -51,10 +59,11 @@ def generate(duration: float, sample_rate: int, channels: int, seed: int, speake
                                 C.c_int(len(speakers)), offs_a.ctypes.data_as(C.c_void_p),
                                 st.ctypes.data_as(C.c_void_p), du.ctypes.data_as(C.c_void_p),
                                 C.c_double(reverb_t60), C.c_double(noise_snr), mix.ctypes.data_as(C.c_void_p),
-                                None, None)
+                                dry.ctypes.data_as(C.c_void_p) if with_sources else None,
+                                img.ctypes.data_as(C.c_void_p) if with_sources else None)
     if rc != 0:
-        raise ValueError(lib.gss_synth_last_error().decode())
-    return mix
+        raise SpecError(lib.gss_synth_last_error().decode())
+    return (mix, dry, img) if with_sources else mix
 
 
 @dataclass

@@ -55,7 +55,7 @@ def check_against_oracle(got, want, label=""):
 
 
 def test_enhance_tiny_batch_with_wpe(gss, oracle):
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     w = synth.workload("tiny")
     res = gss.scheduler.enhance_batches(w.segments, w.cfg, diagnostics=True)
     for i, (ss, r) in enumerate(zip(w.segments, res)):
@@ -64,7 +64,7 @@ def test_enhance_tiny_batch_with_wpe(gss, oracle):
 
 def test_enhance_cfg1_no_wpe(gss, oracle):
     # BASELINE configs[0]: 2 speakers, 7 channels, 10 s, 512-point STFT, 20 iterations, no WPE
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     w = synth.workload("cfg1")
     r = gss.scheduler.enhance_batch(w.segments[0], w.cfg, diagnostics=True)
     assert r.frames == 1251 and len(r.outputs[0]) == 160000
@@ -74,7 +74,7 @@ def test_enhance_cfg1_no_wpe(gss, oracle):
 def test_enhance_ragged_batch_mixed_shapes(gss, oracle):
     # different M, K, N in one call: results must equal one-at-a-time calls bit for bit (batch invariance,
     # the analogue of the reference's worker-count invariance, test_scheduler.cpp:376-407)
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     from paper_2212_05271_b200.gss import scheduler, stft, wpe
     cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(6, 2, 2, 0, 1e-10), True, 6)
     segs = [synth.make_supersegment(900, 4, 2, 2.0, 1.0, cfg), synth.make_supersegment(901, 8, 4, 1.5, 0.5, cfg),
@@ -88,7 +88,7 @@ def test_enhance_ragged_batch_mixed_shapes(gss, oracle):
 
 
 def test_enhance_multi_part_cut_and_failure_isolation(gss, oracle):
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     from paper_2212_05271_b200.gss import scheduler, stft, wpe, manifests
     cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(), False, 4)
     good = synth.make_supersegment(950, 3, 2, 2.0, 1.0, cfg)
@@ -112,7 +112,7 @@ def test_enhance_multi_part_cut_and_failure_isolation(gss, oracle):
 
 def test_resident_batch_matches_one_shot(gss):
     # upload / run / fetch == enhance_batch, and re-running a resident batch is bit-stable
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     w = synth.workload("tiny")
     one = gss.scheduler.enhance_batches(w.segments, w.cfg)
     rb = gss.scheduler.ResidentBatch(w.segments, w.cfg, pinned=True).upload()
@@ -132,7 +132,7 @@ def test_resident_batch_matches_one_shot(gss):
 def test_upload_waves_do_not_change_the_result(gss, monkeypatch):
     # enhance_batch uploads the audio in waves (STFT + WPE of a wave run under the next wave's copy); a segment's
     # result does not depend on its wave, on the number of waves, or on pinned vs pageable host memory
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     w = synth.workload("tiny", n_segments=5)
     monkeypatch.setenv("GSS_B200_WAVES", "1")
     one_wave = gss.scheduler.enhance_batches(w.segments, w.cfg, gss.Context(0))
@@ -261,7 +261,7 @@ def test_enhance_cfg3_shape_ami_8ch_5class(gss, oracle):
     # BASELINE configs[2]: AMI-shaped, 8 channels, 4 speakers + noise, WPE taps 10 / delay 3, 20 iterations,
     # 40 s window. Two of the 257 bins (6.6 - 6.9 kHz, almost no speech energy) are chaotic over 20 EM
     # iterations: the oracle flips their masks under a 1e-7 perturbation of ITS OWN input.
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     w = synth.workload("cfg3", n_segments=1)
     ss, cfg = w.segments[0], w.cfg
     got = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
@@ -276,7 +276,7 @@ def test_enhance_sweep_shapes_channels_and_iterations(gss, oracle, channels, spe
     # BASELINE configs[4] in miniature: channels 2-8, 2-4 speakers (+ noise), 5-40 EM iterations, WPE on, 4 s
     # of target speech in a 20 s window. Every (M, K) pair takes its own kernel specialisation (lanes per
     # frame, class tier). 40 iterations leave more bins chaotic in FP32 (for the oracle too) than 20 do.
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     from paper_2212_05271_b200.gss import scheduler, stft, wpe
     cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(10, 2, 3, 0, 1e-10), True,
                                    iterations)

@@ -27,7 +27,7 @@ def fast_config(gss, out_dir, workers=0):  # test_scheduler.cpp:27-36
 
 def save_fixture(gss, root, name, duration, channels, seed, speakers):
     """A synthetic reverberant mixture as one WAV + its manifests (the role of synthbench::save_fixture)."""
-    from paper_2212_05271_b200 import synth
+    import synthbench as synth
     mf = gss.manifests
     os.makedirs(root, exist_ok=True)
     layout = [ivals for _, ivals in speakers]

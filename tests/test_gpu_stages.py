@@ -152,7 +152,7 @@ def test_wpe_long_prediction_delay(gss, oracle, m, taps, delay):
     want = oracle.wpe(y, oracle.wpe_cfg(taps, delay, 2, 0, 1e-10))
     assert rel_fro(got, want) < 1e-4, rel_fro(got, want)
     # the echo is predictable from the delayed taps: the output must be closer to the dry signal than the input
-    assert np.linalg.norm(got - s) < 0.7 * np.linalg.norm(y - s)
+    assert np.linalg.norm(got - s) < 0.8 * np.linalg.norm(y - s)  # the oracle itself: 0.62 - 0.73
 
 
 def test_wpe_eigen_floor_fallback(gss, oracle):

@@ -17,7 +17,8 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2212_05271_b200 import gss, sharding, synth  # noqa: E402
+from paper_2212_05271_b200 import gss, sharding  # noqa: E402
+import synthbench as synth  # noqa: E402
 from paper_2212_05271_b200.gss import scheduler, stft, wpe  # noqa: E402
 
 
