@@ -93,6 +93,9 @@ void* gss_b200_stream(gss_b200_ctx* ctx);
 int64_t gss_b200_launch_count(const gss_b200_ctx* ctx);
 /* Bytes of device memory currently held by the context's workspaces. */
 int64_t gss_b200_device_bytes(const gss_b200_ctx* ctx);
+/* High-water mark of the same since creation (or since the last call with reset != 0): the peak device
+ * footprint of a batch, the number BASELINE configs[3] ("1 GPU memory-bound sizing") asks for. */
+int64_t gss_b200_device_bytes_peak(gss_b200_ctx* ctx, int32_t reset);
 /* Pinned host memory for fast, asynchronous transfers (optional). */
 gss_status gss_b200_host_alloc(int64_t bytes, void** out);
 void gss_b200_host_free(void* p);

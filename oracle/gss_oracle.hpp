@@ -325,6 +325,71 @@ inline InverseLogDet hermitian_inverse_logdet(const CMat& a, long frequency = -1
 /// chunks; entry (m,n) = Sum w y_m conj(y_n) -- numerics.hpp:128-152.
 /// (Eigen forms the full square with a cfloat GEMM; this port forms the lower
 /// triangle with planar float dot products and mirrors it.)
+#ifdef GSS_ORACLE_VECTOR_GRAM
+// TIMING-ONLY variant (bench.py's CPU arm; never the parity checker): the same chunked float Gram with
+// double cross-chunk accumulation, but each dot product runs on kLanes independent partial sums that the
+// compiler maps to SIMD registers (no -ffast-math needed), two rows of the triangle per pass over a column.
+// This is what Eigen's cfloat GEMM buys the reference; the summation order inside a chunk differs from the
+// scalar port below (tests/test_oracle_golden.py::test_vector_gram_variant_agrees bounds the difference).
+inline CMat weighted_gram(const cf* a, int64_t rows, int cols, const float* w,
+                          int64_t chunk = 2048) {
+  constexpr int kLanes = 16;
+  CMat acc(cols, cols);
+  const int64_t pitch = (chunk + kLanes - 1) / kLanes * kLanes;
+  std::vector<float> re(static_cast<size_t>(cols) * pitch), im(static_cast<size_t>(cols) * pitch);
+  for (int64_t t0 = 0; t0 < rows; t0 += chunk) {
+    const int64_t n = std::min<int64_t>(chunk, rows - t0);
+    const int64_t np = (n + kLanes - 1) / kLanes * kLanes;
+    for (int64_t t = 0; t < n; ++t) {
+      const float s = w ? std::sqrt(std::max(0.0f, w[t0 + t])) : 1.0f;
+      const cf* row = a + (t0 + t) * cols;
+      for (int c = 0; c < cols; ++c) {
+        re[static_cast<size_t>(c) * pitch + t] = row[c].real() * s;
+        im[static_cast<size_t>(c) * pitch + t] = row[c].imag() * s;
+      }
+    }
+    for (int c = 0; c < cols; ++c)
+      for (int64_t t = n; t < np; ++t) re[static_cast<size_t>(c) * pitch + t] = im[static_cast<size_t>(c) * pitch + t] = 0.0f;
+    for (int i = 0; i < cols; i += 2) {
+      const bool two = i + 1 < cols;
+      const float* r0 = &re[static_cast<size_t>(i) * pitch];
+      const float* i0 = &im[static_cast<size_t>(i) * pitch];
+      const float* r1 = two ? r0 + pitch : r0;
+      const float* i1 = two ? i0 + pitch : i0;
+      for (int j = 0; j <= (two ? i + 1 : i); ++j) {
+        const float* rj = &re[static_cast<size_t>(j) * pitch];
+        const float* ij = &im[static_cast<size_t>(j) * pitch];
+        float ar0[kLanes] = {0}, ai0[kLanes] = {0}, ar1[kLanes] = {0}, ai1[kLanes] = {0};
+        for (int64_t t = 0; t < np; t += kLanes) {
+          for (int l = 0; l < kLanes; ++l) {
+            const float a_r = rj[t + l], a_i = ij[t + l];
+            ar0[l] += r0[t + l] * a_r + i0[t + l] * a_i;
+            ai0[l] += i0[t + l] * a_r - r0[t + l] * a_i;
+            ar1[l] += r1[t + l] * a_r + i1[t + l] * a_i;
+            ai1[l] += i1[t + l] * a_r - r1[t + l] * a_i;
+          }
+        }
+        float sr0 = 0, si0 = 0, sr1 = 0, si1 = 0;
+        for (int l = 0; l < kLanes; ++l) {
+          sr0 += ar0[l];
+          si0 += ai0[l];
+          sr1 += ar1[l];
+          si1 += ai1[l];
+        }
+        if (j <= i) {
+          acc(i, j) += cd(sr0, si0);
+          if (j != i) acc(j, i) += cd(sr0, -si0);
+        }
+        if (two) {
+          acc(i + 1, j) += cd(sr1, si1);
+          if (j != i + 1) acc(j, i + 1) += cd(sr1, -si1);
+        }
+      }
+    }
+  }
+  return acc;
+}
+#else
 inline CMat weighted_gram(const cf* a, int64_t rows, int cols, const float* w,
                           int64_t chunk = 2048) {
   CMat acc(cols, cols);
@@ -357,6 +422,8 @@ inline CMat weighted_gram(const cf* a, int64_t rows, int cols, const float* w,
   }
   return acc;
 }
+
+#endif  // GSS_ORACLE_VECTOR_GRAM
 
 // ---------------------------------------------------------------------------
 // FFT (stands in for Eigen::FFT<double>, kissfft backend; power-of-two sizes)

@@ -31,8 +31,9 @@ class OracleError(RuntimeError):
         self.frequency = frequency
 
 
-def build(march: str | None = None, out_dir: str | None = None) -> str:
-    """Compile liboracle.so (g++). Returns the path of the built library."""
+def build(march: str | None = None, out_dir: str | None = None, vector_gram: bool = False) -> str:
+    """Compile liboracle.so (g++). Returns the path of the built library. `vector_gram` builds the timing-only
+    variant whose Gram dot products run on SIMD partial sums (-DGSS_ORACLE_VECTOR_GRAM; needs `out_dir`)."""
     env = dict(os.environ)
     args = ["make", "-C", _HERE]
     if march:
@@ -42,6 +43,8 @@ def build(march: str | None = None, out_dir: str | None = None) -> str:
         out = os.path.join(out_dir, "liboracle.so")
         cmd = ["g++", "-O3", f"-march={march or 'x86-64-v3'}", "-std=c++17", "-fPIC", "-pthread",
                "-shared", "-o", out, os.path.join(_HERE, "oracle_capi.cpp")]
+        if vector_gram:
+            cmd.insert(1, "-DGSS_ORACLE_VECTOR_GRAM")
         subprocess.run(cmd, check=True, env=env)
         return out
     subprocess.run(args, check=True, env=env, stdout=subprocess.DEVNULL)

@@ -120,7 +120,7 @@ class SegmentDiag(C.Structure):
 EXPORTS = [
     "gss_b200_default_stft_config", "gss_b200_default_wpe_config", "gss_b200_default_pipeline_config",
     "gss_b200_create", "gss_b200_destroy", "gss_b200_last_error", "gss_b200_last_error_frequency",
-    "gss_b200_stream", "gss_b200_launch_count", "gss_b200_device_bytes", "gss_b200_host_alloc",
+    "gss_b200_stream", "gss_b200_launch_count", "gss_b200_device_bytes", "gss_b200_device_bytes_peak", "gss_b200_host_alloc",
     "gss_b200_host_free", "gss_b200_stft", "gss_b200_istft", "gss_b200_wpe", "gss_b200_unit_normalize",
     "gss_b200_em_fit", "gss_b200_log_likelihood", "gss_b200_mvdr_stats", "gss_b200_select_reference",
     "gss_b200_mvdr", "gss_b200_apply", "gss_b200_enhance_batch", "gss_b200_batch_upload", "gss_b200_batch_run",
@@ -151,6 +151,8 @@ def load():
     lib.gss_b200_launch_count.argtypes = [C.c_void_p]
     lib.gss_b200_device_bytes.restype = C.c_int64
     lib.gss_b200_device_bytes.argtypes = [C.c_void_p]
+    lib.gss_b200_device_bytes_peak.restype = C.c_int64
+    lib.gss_b200_device_bytes_peak.argtypes = [C.c_void_p, C.c_int32]
     lib.gss_b200_frame_count.restype = C.c_int64
     lib.gss_b200_frame_count.argtypes = [C.c_int64, C.c_int32, C.c_int32]
     lib.gss_b200_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]

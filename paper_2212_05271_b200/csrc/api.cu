@@ -58,6 +58,7 @@ struct gss_b200_ctx {
   long long err_freq = -1;
   long long launches = 0;
   long long device_bytes = 0;
+  long long device_bytes_peak = 0;
   std::map<std::pair<int, int>, Tables> tables;
   double stage_ms[GSS_B200_NUM_STAGES] = {0, 0, 0, 0, 0, 0, 0};
   // optional per-kernel device clocks (gss_b200_profile)
@@ -179,6 +180,7 @@ struct DevMem {
     if (last != cudaSuccess) return nullptr;
     blocks.emplace_back(p, bytes);
     c->device_bytes += (long long)bytes;
+    c->device_bytes_peak = std::max(c->device_bytes_peak, c->device_bytes);
     return reinterpret_cast<T*>(p);
   }
   void release() {
@@ -765,6 +767,12 @@ int64_t gss_b200_last_error_frequency(const gss_b200_ctx* c) { return c ? c->err
 void* gss_b200_stream(gss_b200_ctx* c) { return c ? (void*)c->stream : nullptr; }
 int64_t gss_b200_launch_count(const gss_b200_ctx* c) { return c ? c->launches : 0; }
 int64_t gss_b200_device_bytes(const gss_b200_ctx* c) { return c ? c->device_bytes : 0; }
+int64_t gss_b200_device_bytes_peak(gss_b200_ctx* c, int32_t reset) {
+  if (!c) return 0;
+  const long long peak = c->device_bytes_peak;
+  if (reset) c->device_bytes_peak = c->device_bytes;
+  return peak;
+}
 
 gss_status gss_b200_host_alloc(int64_t bytes, void** out) {
   *out = nullptr;

@@ -81,6 +81,16 @@ struct PartLayout {
   static constexpr int CELL = L * STRIDE;
 };
 
+#ifdef GSS_ACCURATE_MATH
+// Measurement variant (tools/variant.py accurate -DGSS_ACCURATE_MATH=1): correctly rounded reciprocal / square
+// root and the full-precision log2f / exp2f in place of the MUFU approximations, and the soft-max sum in double
+// like cacgmm.hpp:239-255. It exists to put a number on how much of the device-vs-oracle mask difference is the
+// fast math (profiles/parity_r02.md); the product build uses the approximations below.
+__device__ __forceinline__ float rcp_approx(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ float lg2_approx(float x) { return log2f(x); }
+__device__ __forceinline__ float ex2_approx(float x) { return exp2f(x); }
+__device__ __forceinline__ float sqrt_approx(float x) { return __fsqrt_rn(x); }
+#else
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -101,6 +111,7 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+#endif  // GSS_ACCURATE_MATH
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>

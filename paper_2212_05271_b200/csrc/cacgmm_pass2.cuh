@@ -253,6 +253,18 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
       u[k] = fmaf(-(float)M, lg2_approx(q[k]), ckp[k]);
       mx = fmaxf(mx, u[k]);
     }
+#ifdef GSS_ACCURATE_MATH
+    double sed = 0.0, ud[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      ud[k] = exp2((double)u[k] - (double)mx);
+      sed += ud[k];
+    }
+    const double rinvd = valid ? 1.0 / sed : 0.0;
+    const float se = (float)sed, rinv = 1.f;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) u[k] = (float)(ud[k] * rinvd);
+#else
     float se = 0.f;
 #pragma unroll
     for (int k = 0; k < KT; ++k) {
@@ -260,6 +272,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
       se += u[k];
     }
     const float rinv = valid ? rcp_approx(se) : 0.f;
+#endif
     // log2 units, scaled once at the end; the common s^2 factor comes back here: -M log2(s^2) = +M log2(nr2)
     // (a lane sums at most T / 256 such terms in float; lanes and chunks are then summed in double)
     if (valid) sums[32 * KT] += mx + lg2_approx(se) + (float)M * lg2_approx(nr2);

@@ -36,6 +36,10 @@ class Context:
     def device_bytes(self) -> int:
         return int(self.lib.gss_b200_device_bytes(self.handle))
 
+    def device_bytes_peak(self, reset: bool = False) -> int:
+        """High-water mark of the workspaces since creation / the last reset."""
+        return int(self.lib.gss_b200_device_bytes_peak(self.handle, C.c_int32(1 if reset else 0)))
+
     def stage_ms(self) -> dict:
         ms = (C.c_double * capi.NUM_STAGES)()
         self.check(self.lib.gss_b200_stage_ms(self.handle, ms))

@@ -167,3 +167,38 @@ def workload(name: str, n_segments: int | None = None, first: int = 0, threads: 
     out_s = sum((p.sample_end - p.sample_begin) / sr for s in segs for p in s.parts)
     asm_s = sum(s.audio.num_samples() / sr for s in segs)
     return Workload(name, cfg, segs, out_s, asm_s)
+
+
+def sweep_params(total: int = 4096, seed: int = 5000):
+    """BASELINE configs[4]: `total` segments, target durations U[2,12] s + 2 x 15 s context,
+    2-8 channels, 2-4 speakers (+ noise class), 5/10/20/40 EM iterations, WPE on. Returns one
+    (seed, channels, speakers, target seconds, iterations) tuple per segment; cheap, so every rank can draw the
+    whole list and generate only the audio of the segments it owns."""
+    rng = np.random.RandomState(seed)
+    out = []
+    for i in range(total):
+        iters = int(rng.choice([5, 10, 20, 40]))
+        out.append((seed + i, int(rng.randint(2, 9)), int(rng.randint(2, 5)), float(rng.uniform(2.0, 12.0)), iters))
+    return out
+
+
+def sweep_cfg(iters: int) -> scheduler.PipelineConfig:
+    return _cfg(True, 2, iters)
+
+
+def sweep_frames(target_dur: float, context: float = 15.0, cfg: scheduler.PipelineConfig | None = None) -> int:
+    cfg = cfg or _cfg()
+    n = int(math.floor((target_dur + 2 * context) * cfg.stft.sample_rate + 0.5))
+    return stft.frame_count(n, cfg.stft)
+
+
+def make_sweep_segments(params, threads: int = 8):
+    """SuperSegments for a list of sweep_params() entries, generated on `threads` host threads."""
+    _load()
+
+    def mk(p):
+        seed, m, k, dur, iters = p
+        return make_supersegment(seed, m, k, dur, 15.0, sweep_cfg(iters))
+
+    with ThreadPoolExecutor(max_workers=max(1, min(threads, len(params) or 1))) as ex:
+        return list(ex.map(mk, params))

@@ -580,3 +580,23 @@ def test_assemble_clips_context(oracle):
     assert a.context_left == pytest.approx(0.2) and a.context_right == pytest.approx(1.0)
     b = oracle.assemble_indices([(3.5, 0.5)], sr, 4 * sr, 1.0)
     assert b.context_left == pytest.approx(1.0) and b.context_right == pytest.approx(0.0)
+
+
+def test_vector_gram_variant_agrees(oracle, tmp_path):
+    """bench.py times the oracle built with -DGSS_ORACLE_VECTOR_GRAM (SIMD partial sums in the Gram, what Eigen's
+    cfloat GEMM gives the reference). Same chunks, same double accumulation across chunks; only the float
+    summation order inside a chunk differs, so the two builds agree to float rounding."""
+    rng = np.random.RandomState(7)
+    a = (rng.randn(5000, 11) + 1j * rng.randn(5000, 11)).astype(np.complex64)
+    w = rng.rand(5000).astype(np.float32)
+    want = oracle.weighted_gram(a, w)
+    want_unit = oracle.weighted_gram(a[:37, :3])
+    try:
+        oracle.load(oracle.build(out_dir=str(tmp_path), vector_gram=True))
+        got = oracle.weighted_gram(a, w)
+        got_unit = oracle.weighted_gram(a[:37, :3])
+    finally:
+        oracle.load(oracle._LIB_PATH)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-6
+    assert np.linalg.norm(got_unit - want_unit) / np.linalg.norm(want_unit) < 1e-6
+    assert np.allclose(got, got.conj().T)

@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 WL=${WL:-cfg2}; SEGS=${SEGS:-16}
 for tag in "$@"; do
   if [ "$tag" = base ]; then unset GSS_B200_LIB; else export GSS_B200_LIB=$PWD/paper_2212_05271_b200/lib/libgss_b200_$tag.so; fi
-  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --workload $WL --segments $SEGS > gpurun_out/exp_$tag.log 2>&1
+  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --headline-only --workload $WL --segments $SEGS > gpurun_out/exp_$tag.log 2>&1
   python - "$tag" <<'PY'
 import json, sys
 tag = sys.argv[1]
