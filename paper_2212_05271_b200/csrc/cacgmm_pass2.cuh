@@ -49,9 +49,22 @@ struct EmPass2Cfg {
   static constexpr int NA = FINAL ? 2 : KT;
   static constexpr int WS = FINAL ? 2 : KTP;       // weights parked per frame
   static constexpr int SPW = 32 / L;               // frames per phase-B step
+  /// Column swizzle of the dof scratch. SPW >= 8: a phase-B quarter-warp is 8 frames of one slice, the identity
+  /// does it. SPW = 4 (L = 8): a quarter-warp is 4 frames x 2 slices whose chunk numbers differ in bit 1 (CPG = 2),
+  /// so the frame's bit 1 must land elsewhere: bits (0, 1, 2) -> (0, 2, 1). With the identity these loads were
+  /// 2-way conflicted (41 M conflict cycles per cfg3 sweep).
+  __host__ __device__ static constexpr unsigned swz(unsigned fr) {
+    return (L == 8 && NDOFP == 8 ? ((fr & 1u) | ((fr & 2u) << 1) | ((fr & 4u) >> 1) | (fr & ~7u)) : fr) & (unsigned)(NCHP - 1);
+  }
   static constexpr int NW = kEmThreads / 32;
-  static constexpr int COEF_FLOATS = L * NDOFP * KTP;
-  static constexpr int YSTAGE_FLOATS = 32 * M * 2;  // one group of frames (cp.async landing zone)
+  // coefficient table of one lane slice: [dof][class] packed (no class padding), rounded up to whole float4s
+  static constexpr int CS = (NDOFP * KT + 3) & ~3;
+  static constexpr int COEF_FLOATS = L * CS;
+  // one group of frames (cp.async landing zone). Frame stride in float2 units: odd, so that the 16 lanes of a
+  // half-warp reading channel m of their own frame (LDS.64) fall into 16 different bank pairs. With the natural
+  // stride M = 8 they fell into two (8-way conflict: 72 M conflict cycles per cfg3 sweep, profiles/ncu_full_r02.md)
+  static constexpr int SY = (M % 2 == 0) ? M + 1 : M;
+  static constexpr int YSTAGE_FLOATS = 32 * SY * 2;
   // per warp: dof scratch [32][NCHP] float4 | weights [32][WS] | two frame stages; a multiple of 256 bytes
   static constexpr int SUMS = KT + 1;  // per frame lane: class masses and the log-likelihood, kept out of registers
   static constexpr int WARP_SCRATCH_FLOATS = (32 * NCHP * 4 + 32 * WS + 2 * YSTAGE_FLOATS + 32 * SUMS + 63) & ~63;
@@ -76,7 +89,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   constexpr bool CPG_POW2 = (CPG & (CPG - 1)) == 0;
   using PL = PartLayout<M, L, KT, NA>;
   extern __shared__ float4 smem_f4[];
-  float* s_coef = reinterpret_cast<float*>(smem_f4);          // [g][idx][KTP]
+  float* s_coef = reinterpret_cast<float*>(smem_f4);          // [g][idx * KT + k], CS floats per g
   float* s_ck = s_coef + Cfg::COEF_FLOATS;                    // [pattern][KTP]
   const int ck_floats = (a.npat_max * KTP + 3) & ~3;
   float* s_scratch = s_ck + ck_floats;                        // NW x WARP_SCRATCH_FLOATS, 256-byte aligned:
@@ -97,8 +110,8 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   {
     const float* cp = a.coef + sd.coef_off + (long long)f * L * (KT * NDOF);  // [g][k][j]
     for (int i = tid; i < Cfg::COEF_FLOATS; i += kEmThreads) {
-      const int k = i % KTP, gj = i / KTP, j = gj % NDOFP, g = gj / NDOFP;
-      s_coef[i] = (k < KT && j < NDOF) ? cp[(g * KT + k) * NDOF + j] : 0.f;
+      const int g = i / Cfg::CS, r = i - g * Cfg::CS, j = r / KT, k = r - j * KT;
+      s_coef[i] = j < NDOF ? cp[(g * KT + k) * NDOF + j] : 0.f;
     }
     const float* cks = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
     for (int i = tid; i < sd.npat * KTP; i += kEmThreads) {
@@ -117,15 +130,17 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
 
   float* wscr = s_scratch + warp * Cfg::WARP_SCRATCH_FLOATS;
   float* wbuf = wscr + 32 * NCHP * 4;                                     // [32][WS]
-  float2* ybuf = reinterpret_cast<float2*>(wbuf + 32 * WS);               // [2][32 * M]
-  float* sums = reinterpret_cast<float*>(ybuf + 2 * 32 * M) + lane;       // [SUMS][32], this lane's column
+  float2* ybuf = reinterpret_cast<float2*>(wbuf + 32 * WS);               // [2][32][SY]
+  float* sums = reinterpret_cast<float*>(ybuf + 2 * 32 * Cfg::SY) + lane;  // [SUMS][32], this lane's column
 #pragma unroll
   for (int k = 0; k < Cfg::SUMS; ++k) sums[32 * k] = 0.f;
   const int g = lane / SPW, slot = lane % SPW;  // phase-B role
-  // Dof scratch addressing: chunk c of frame fr lives at float4 position fr * NCHP + (c ^ (fr % NCHP)); with
-  // the scratch aligned to the frame stride that is (address of chunk 0's home) XOR (c * 16): one LOP3.
+  // Dof scratch addressing: chunk c of frame fr lives at float4 position fr * NCHP + (c ^ swz(fr)); with the
+  // scratch aligned to the frame stride that is (address of chunk 0's home) XOR (c * 16): one LOP3. swz is a
+  // permutation of the frame number's low bits (Cfg::swz) chosen so that the 8 lanes of a quarter-warp hit 8
+  // different 16-byte columns in phase A (8 frames, one chunk) AND in phase B (SPW frames x 8 / SPW slices).
   const unsigned pbase = (unsigned)__cvta_generic_to_shared(wscr);
-  const unsigned pa_store = pbase + (unsigned)lane * (NCHP * 16) + ((unsigned)lane & (NCHP - 1)) * 16;
+  const unsigned pa_store = pbase + (unsigned)lane * (NCHP * 16) + Cfg::swz((unsigned)lane) * 16;
 
   float acc[NA][NDOF];
 #pragma unroll
@@ -141,12 +156,12 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   // frames of group `grp` -> stage `st` of this warp's landing zone; frames past the end are zero
   auto issue_group = [&](int grp, int st) {
     const float2* gs = src + (long long)grp * 32 * M;
-    float2* d = ybuf + st * (32 * M);
+    float2* d = ybuf + st * (32 * Cfg::SY);
     const int n = (nt - grp * 32) * M;  // valid elements (may exceed 32 * M)
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       const int i = lane + 32 * j;
-      cp_async8_zfill(d + i, gs + (i < n ? i : 0), i < n);
+      cp_async8_zfill(d + i + (Cfg::SY - M) * (i / M), gs + (i < n ? i : 0), i < n);
     }
     cp_async_commit();
   };
@@ -173,7 +188,7 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
     __syncwarp();
     float2 y[M];
     {
-      const float2* ys = ybuf + (it & 1) * (32 * M) + lane * M;
+      const float2* ys = ybuf + (it & 1) * (32 * Cfg::SY) + lane * Cfg::SY;
 #pragma unroll
       for (int m = 0; m < M; ++m) y[m] = ys[m];
     }
@@ -188,6 +203,8 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
       float pg[NDOFP];
 #pragma unroll
       for (int j = 0; j < NDOFP; ++j) pg[j] = 0.f;
+      float4 cc = make_float4(0.f, 0.f, 0.f, 0.f);
+      int have = -1;
 #pragma unroll
       for (int i = 0; i < Lay::RPL; ++i) {
         const int row = gg + i * L;
@@ -207,20 +224,17 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
               p = row < M / 2 ? fmaf(x.x, z.x, x.y * z.y) : fmaf(x.y, z.x, -(x.x * z.y));
             }
             pg[i * M + jr] = p;
-            const float* c = s_coef + (gg * NDOFP + i * M + jr) * KTP;  // warp-uniform address: broadcast
-            if (KTP == 2) {
-              const float2 c2 = *reinterpret_cast<const float2*>(c);
-              q[0] = fmaf(c2.x, p, q[0]);
-              if (KT > 1) q[KT > 1 ? 1 : 0] = fmaf(c2.y, p, q[KT > 1 ? 1 : 0]);
-            } else {
+            // packed coefficients: element e = dof * KT + k of this slice, fetched as whole float4s through a
+            // warp-uniform (broadcast) address; `have` and every select below fold at compile time
 #pragma unroll
-              for (int k4 = 0; k4 < KTP / 4; ++k4) {
-                const float4 c4 = reinterpret_cast<const float4*>(c)[k4];
-                if (4 * k4 + 0 < KT) q[4 * k4 + 0 < KT ? 4 * k4 + 0 : 0] = fmaf(c4.x, p, q[4 * k4 + 0 < KT ? 4 * k4 + 0 : 0]);
-                if (4 * k4 + 1 < KT) q[4 * k4 + 1 < KT ? 4 * k4 + 1 : 0] = fmaf(c4.y, p, q[4 * k4 + 1 < KT ? 4 * k4 + 1 : 0]);
-                if (4 * k4 + 2 < KT) q[4 * k4 + 2 < KT ? 4 * k4 + 2 : 0] = fmaf(c4.z, p, q[4 * k4 + 2 < KT ? 4 * k4 + 2 : 0]);
-                if (4 * k4 + 3 < KT) q[4 * k4 + 3 < KT ? 4 * k4 + 3 : 0] = fmaf(c4.w, p, q[4 * k4 + 3 < KT ? 4 * k4 + 3 : 0]);
+            for (int k = 0; k < KT; ++k) {
+              const int e = (i * M + jr) * KT + k;
+              if ((e >> 2) != have) {
+                cc = reinterpret_cast<const float4*>(s_coef + gg * Cfg::CS)[e >> 2];
+                have = e >> 2;
               }
+              const float cv = (e & 3) == 0 ? cc.x : (e & 3) == 1 ? cc.y : (e & 3) == 2 ? cc.z : cc.w;
+              q[k] = fmaf(cv, p, q[k]);
             }
           }
         }
@@ -313,35 +327,42 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
     __syncwarp();
 
     // ================= phase B: lane = (frame slot, dof slice g) =================
-#pragma unroll
-    for (int step = 0; step < L; ++step) {
+    // Register double buffering: the dofs and weights of step + 1 are requested before the FMAs of step. The loads
+    // are volatile asm on purpose: as plain loads the compiler sank each class's weight into that class's
+    // conditional block, and every block then began with a shared-memory round trip (short-scoreboard stalls were
+    // 58 % of this phase's samples on cfg3, profiles/ncu_full_r02.md).
+    auto load_step = [&](int step, float (&pv)[NDOFP], float (&w)[WS]) {
       const int fr = step * SPW + slot;
       const unsigned pa_load =
-          (pbase + (unsigned)fr * (NCHP * 16) + ((unsigned)fr & (NCHP - 1)) * 16) ^ (unsigned)(g * CPG * 16);
-      float pv[NDOFP];
+          (pbase + (unsigned)fr * (NCHP * 16) + Cfg::swz((unsigned)fr) * 16) ^ (unsigned)(g * CPG * 16);
 #pragma unroll
       for (int c = 0; c < CPG; ++c)  // (g * CPG + c) ^ x == (g * CPG) ^ c ^ x when CPG is a power of two ...
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(pv[4 * c]), "=f"(pv[4 * c + 1]), "=f"(pv[4 * c + 2]), "=f"(pv[4 * c + 3])
                      : "r"(CPG_POW2 ? (pa_load ^ (unsigned)(c * 16))
-                                    : ((pbase + (unsigned)fr * (NCHP * 16) + ((unsigned)fr & (NCHP - 1)) * 16) ^
+                                    : ((pbase + (unsigned)fr * (NCHP * 16) + Cfg::swz((unsigned)fr) * 16) ^
                                        (unsigned)((g * CPG + c) * 16)))
                      : "memory");
-      float w[WS];
+      const unsigned wa = pbase + (unsigned)(32 * NCHP * 16) + (unsigned)fr * (WS * 4);
       if (WS == 2) {
-        const float2 v = *reinterpret_cast<const float2*>(wbuf + fr * WS);
-        w[0] = v.x;
-        w[1] = v.y;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(w[0]), "=f"(w[WS > 1 ? 1 : 0]) : "r"(wa) : "memory");
       } else {
 #pragma unroll
-        for (int k4 = 0; k4 < WS / 4; ++k4) {
-          const float4 v = reinterpret_cast<const float4*>(wbuf + fr * WS)[k4];
-          w[4 * k4] = v.x;
-          w[4 * k4 + 1] = v.y;
-          w[4 * k4 + 2] = v.z;
-          w[4 * k4 + 3] = v.w;
-        }
+        for (int k4 = 0; k4 < WS / 4; ++k4)
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(w[WS >= 4 ? 4 * k4 : 0]), "=f"(w[WS >= 4 ? 4 * k4 + 1 : 0]),
+                         "=f"(w[WS >= 4 ? 4 * k4 + 2 : 0]), "=f"(w[WS >= 4 ? 4 * k4 + 3 : 0])
+                       : "r"(wa + (unsigned)(16 * k4))
+                       : "memory");
       }
+    };
+    float pvb[2][NDOFP], wb[2][WS];
+    load_step(0, pvb[0], wb[0]);
+#pragma unroll
+    for (int step = 0; step < L; ++step) {
+      const float(&pv)[NDOFP] = pvb[step & 1];
+      const float(&w)[WS] = wb[step & 1];
+      if (step + 1 < L) load_step(step + 1, pvb[(step + 1) & 1], wb[(step + 1) & 1]);
       if (FINAL) {
 #pragma unroll
         for (int j = 0; j < NDOF; ++j) {

