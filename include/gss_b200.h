@@ -225,6 +225,38 @@ gss_status gss_b200_profile(gss_b200_ctx* ctx, int32_t enable);
 gss_status gss_b200_kernel_ms(gss_b200_ctx* ctx, double* ms /* [GSS_B200_NUM_KERNELS] */,
                               int64_t* launches /* [GSS_B200_NUM_KERNELS] */);
 
+/* ---- device-pointer variants ("All pointers are host pointers unless the _dev variant is used") --
+ * For callers whose tensors already live in HBM (a loader that decodes on the GPU, a downstream ASR front end).
+ * Every tensor argument is a DEVICE pointer on the context's device; small control arrays stay on the host where
+ * noted. `stream` is the caller's cudaStream_t (NULL = legacy default stream): the operator is ordered after the
+ * work already queued on it, and the stream waits for the operator's results -- the stage operators below do not
+ * synchronise with the host (gss_b200_wpe_dev reads back one status word, a solve can fail). Same return codes,
+ * same kernels, same bits as the host variants. */
+gss_status gss_b200_stft_dev(gss_b200_ctx* ctx, const float* audio_dev, int32_t channels, int64_t num_samples,
+                             int32_t signal_rate, const gss_stft_config* cfg, float* out_ftm_dev, void* stream);
+gss_status gss_b200_istft_dev(gss_b200_ctx* ctx, const float* spec_ftm_dev, int32_t bins, int64_t frames,
+                              int32_t channels, int64_t num_samples, const gss_stft_config* cfg, float* out_dev,
+                              void* stream);
+gss_status gss_b200_wpe_dev(gss_b200_ctx* ctx, const float* in_ftm_dev, int32_t bins, int64_t frames,
+                            int32_t channels, const gss_wpe_config* cfg, float* out_ftm_dev, void* stream);
+gss_status gss_b200_unit_normalize_dev(gss_b200_ctx* ctx, const float* in_ftm_dev, int32_t bins, int64_t frames,
+                                       int32_t channels, float* out_ftm_dev, void* stream);
+/* h_fm is a HOST array (F x M cdouble, the value mvdr returned); y and out are device tensors. */
+gss_status gss_b200_apply_dev(gss_b200_ctx* ctx, const double* h_fm, int32_t h_bins, int32_t h_channels,
+                              const float* y_ftm_dev, int32_t bins, int64_t frames, int32_t channels,
+                              float* out_ft_dev, void* stream);
+/* scheduler::enhance_batch with the audio and the outputs in HBM: in every gss_segment_desc `audio`, `out_wave`
+ * and the optional `mono_out` / `gamma_out` / `h_out` are DEVICE pointers; `activity`, `part_begin`, `part_end`
+ * and `out_lengths` stay HOST arrays (a few KB of integers the host planner produced). Per-segment status comes
+ * back in `diags`, so the call returns after the batch has finished. */
+gss_status gss_b200_enhance_batch_dev(gss_b200_ctx* ctx, int32_t n_segments, const gss_segment_desc* segments,
+                                      const gss_pipeline_config* cfg, gss_segment_diag* diags, void* stream);
+
+/* NVTX: every stage of enhance_batch is enqueued inside a host-side range named after the reference's stage keys
+ * ("gss.stft", "gss.wpe", "gss.mask", "gss.beamform", "gss.istft", "gss.d2h", all inside "gss.enhance_batch"), so
+ * a profiler attributes the launches to the stage. Returns how many ranges this context has opened. */
+int64_t gss_b200_nvtx_range_count(const gss_b200_ctx* ctx);
+
 /* ---- host-only helpers (bit-exact integer / scalar forms; no context) ---- */
 
 /* stft::frame_count (stft.hpp:120-124) */

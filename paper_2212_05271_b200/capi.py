@@ -127,6 +127,8 @@ EXPORTS = [
     "gss_b200_batch_fetch", "gss_b200_batch_free", "gss_b200_stage_ms", "gss_b200_profile", "gss_b200_kernel_ms", "gss_b200_fp32_peak", "gss_b200_frame_count",
     "gss_b200_build_activity_at", "gss_b200_assemble_indices", "gss_b200_cacg_log_pdf",
     "gss_b200_time_varying_weights",
+    "gss_b200_stft_dev", "gss_b200_istft_dev", "gss_b200_wpe_dev", "gss_b200_unit_normalize_dev", "gss_b200_apply_dev",
+    "gss_b200_enhance_batch_dev", "gss_b200_nvtx_range_count",
 ]
 
 _lib = None
@@ -151,6 +153,8 @@ def load():
     lib.gss_b200_launch_count.argtypes = [C.c_void_p]
     lib.gss_b200_device_bytes.restype = C.c_int64
     lib.gss_b200_device_bytes.argtypes = [C.c_void_p]
+    lib.gss_b200_nvtx_range_count.restype = C.c_int64
+    lib.gss_b200_nvtx_range_count.argtypes = [C.c_void_p]
     lib.gss_b200_device_bytes_peak.restype = C.c_int64
     lib.gss_b200_device_bytes_peak.argtypes = [C.c_void_p, C.c_int32]
     lib.gss_b200_frame_count.restype = C.c_int64

@@ -15,6 +15,8 @@
 #include <vector>
 
 #include "../../include/gss_b200.h"
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.h"
 
 namespace gssb {
@@ -74,6 +76,8 @@ struct gss_b200_ctx {
   int wpe_apply_tc = 1;      // GSS_B200_WPE_APPLY=fp32 selects the FP32-FMA prediction kernel instead of tcgen05
   int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
   int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
+  bool dev_call = false;     // inside a *_dev entry point: tensors are device memory, completion is an event
+  long long nvtx_ranges = 0; // NVTX ranges opened by this context (gss_b200_nvtx_range_count)
 };
 
 namespace {
@@ -106,6 +110,53 @@ struct KClock {
     if (b) cudaEventRecord(b, c->stream);
   }
 };
+/// NVTX range on the calling host thread, named after the reference's stage keys ("gss.stft", "gss.wpe", ...):
+/// a profiler attributes the launches enqueued inside it to the stage. No tool attached = two empty calls.
+struct NvtxRange {
+  NvtxRange(gss_b200_ctx* c, const char* name) {
+    if (c) ++c->nvtx_ranges;
+    nvtxRangePushA(name);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+/// End of a stage entry point: the host variants return finished results; the *_dev variants return as soon as
+/// the work is queued (DevCall makes the caller's stream wait for it).
+inline cudaError_t finish_call(gss_b200_ctx* c) { return c->dev_call ? cudaSuccess : cudaStreamSynchronize(c->stream); }
+
+/// Scope of a *_dev entry point: the context stream first waits for everything queued on the caller's stream,
+/// and on exit the caller's stream waits for everything the call queued. No host synchronisation.
+struct DevCall {
+  gss_b200_ctx* c;
+  cudaStream_t user;
+  cudaEvent_t ev = nullptr;
+  DevCall(gss_b200_ctx* ctx, void* stream) : c(ctx), user(reinterpret_cast<cudaStream_t>(stream)) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    c->dev_call = true;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+      ev = nullptr;
+      return;
+    }
+    cudaEventRecord(ev, user);
+    cudaStreamWaitEvent(c->stream, ev, 0);
+    cudaStreamWaitEvent(c->copy_stream, ev, 0);  // enhance_batch moves the audio on its copy stream
+  }
+  ~DevCall() {
+    if (!c) return;
+    c->dev_call = false;
+    if (ev) {
+      cudaEventRecord(ev, c->stream);
+      cudaStreamWaitEvent(user, ev, 0);
+      cudaEventDestroy(ev);
+    } else {
+      cudaStreamSynchronize(c->stream);  // no event: fall back to a host wait, never to unordered work
+    }
+  }
+};
+
 /// A pair of timing events destroyed on every exit path.
 struct EventPair {
   cudaEvent_t a = nullptr, b = nullptr;
@@ -219,10 +270,10 @@ gss_status get_tables(gss_b200_ctx* c, const gss_stft_config& s, Tables& out) {
   CU_TRY(c, cudaMalloc(&t.win, sizeof(float) * n));
   CU_TRY(c, cudaMalloc(&t.tw_d, sizeof(double2) * (n / 2)));
   CU_TRY(c, cudaMalloc(&t.win_d, sizeof(double) * n));
-  CU_TRY(c, cudaMemcpyAsync(t.tw, tw.data(), sizeof(float2) * (n / 2), cudaMemcpyHostToDevice, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(t.win, win.data(), sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(t.tw_d, tw_d.data(), sizeof(double2) * (n / 2), cudaMemcpyHostToDevice, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(t.win_d, win_d.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(t.tw, tw.data(), sizeof(float2) * (n / 2), cudaMemcpyDefault, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(t.win, win.data(), sizeof(float) * n, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(t.tw_d, tw_d.data(), sizeof(double2) * (n / 2), cudaMemcpyDefault, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(t.win_d, win_d.data(), sizeof(double) * n, cudaMemcpyDefault, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   c->tables[key] = t;
   out = t;
@@ -456,15 +507,15 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
     return fail(c, GSS_CUDA_ERROR, why);
   }
   cudaStream_t st = c->stream;
-  CU_TRY(c, cudaMemcpyAsync(g.d_segs, g.segs.data(), sizeof(SegDev) * g.nseg, cudaMemcpyHostToDevice, st));
+  CU_TRY(c, cudaMemcpyAsync(g.d_segs, g.segs.data(), sizeof(SegDev) * g.nseg, cudaMemcpyDefault, st));
   if (!work.empty())
-    CU_TRY(c, cudaMemcpyAsync(g.d_work, work.data(), sizeof(WorkItem) * work.size(), cudaMemcpyHostToDevice, st));
+    CU_TRY(c, cudaMemcpyAsync(g.d_work, work.data(), sizeof(WorkItem) * work.size(), cudaMemcpyDefault, st));
   CU_TRY(c, cudaMemsetAsync(g.status, 0xFF, sizeof(status_t) * g.nseg, st));
   CU_TRY(c, cudaMemsetAsync(g.zeroed, 0, sizeof(int) * g.nseg, st));
   CU_TRY(c, cudaMemsetAsync(g.ref, 0, sizeof(int) * g.nseg, st));
   if (need.em && !h_pat.empty()) {
-    CU_TRY(c, cudaMemcpyAsync(g.pat, h_pat.data(), h_pat.size(), cudaMemcpyHostToDevice, st));
-    CU_TRY(c, cudaMemcpyAsync(g.masks, h_masks.data(), sizeof(uint32_t) * h_masks.size(), cudaMemcpyHostToDevice, st));
+    CU_TRY(c, cudaMemcpyAsync(g.pat, h_pat.data(), h_pat.size(), cudaMemcpyDefault, st));
+    CU_TRY(c, cudaMemcpyAsync(g.masks, h_masks.data(), sizeof(uint32_t) * h_masks.size(), cudaMemcpyDefault, st));
   }
   // pageable sources above (std::vector) are consumed synchronously by cudaMemcpyAsync's
   // staging, so they may go out of scope on return.
@@ -666,7 +717,7 @@ gss_status copy_wave(gss_b200_ctx* c, gss_b200_batch* b, Group& g, int w) {
   for (int j = g.wave_first[w]; j < g.wave_first[w + 1]; ++j) {
     const gss_segment_desc& d = b->desc[g.members[j]];
     CU_TRY(c, cudaMemcpyAsync(g.audio + g.segs[j].audio_off, d.audio,
-                              sizeof(float) * (size_t)d.channels * d.num_samples, cudaMemcpyHostToDevice,
+                              sizeof(float) * (size_t)d.channels * d.num_samples, cudaMemcpyDefault,
                               c->copy_stream));
   }
   CU_TRY(c, cudaEventRecord(g.wave_ev[w], c->copy_stream));
@@ -1020,6 +1071,7 @@ gss_status run_impl(gss_b200_ctx* c, gss_b200_batch* b) {
       for (int v = resident ? 0 : w; v <= (resident ? g.num_waves() - 1 : w); ++v)
         CU_TRY(c, cudaStreamWaitEvent(st, g.wave_ev[v], 0));
       {
+        NvtxRange nv(c, "gss.stft");
         StftArgs a;
         a.audio = g.audio;
         a.y = g.Y;
@@ -1035,6 +1087,7 @@ gss_status run_impl(gss_b200_ctx* c, gss_b200_batch* b) {
       }
       cudaEventRecord(g.marks[2 * w], st);
       if (cfg.enable_wpe) {
+        NvtxRange nv(c, "gss.wpe");
         gss_status rc = run_wpe(c, g, cfg.wpe, first, count);
         if (rc != GSS_OK) return rc;
       }
@@ -1049,12 +1102,14 @@ gss_status run_impl(gss_b200_ctx* c, gss_b200_batch* b) {
     cudaEventRecord(ev[1], st);
     cudaEventRecord(ev[2], st);
     {
+      NvtxRange nv(c, "gss.mask");
       EmRun r{tensor, 1, true, false, false};
       gss_status rc = run_em(c, g, r);
       if (rc != GSS_OK) return rc;
     }
     cudaEventRecord(ev[3], st);
     {
+      NvtxRange nv(c, "gss.beamform");
       StatsFinalArgs sf;
       sf.segs = g.d_segs;
       sf.part = g.part;
@@ -1082,6 +1137,7 @@ gss_status run_impl(gss_b200_ctx* c, gss_b200_batch* b) {
     }
     cudaEventRecord(ev[4], st);
     {
+      NvtxRange nv(c, "gss.istft");
       IstftArgs ia;
       ia.x = g.X;
       ia.wave = g.wave;
@@ -1113,6 +1169,7 @@ gss_status gss_b200_batch_run(gss_b200_ctx* c, gss_b200_batch* b) { return run_i
 gss_status gss_b200_batch_fetch(gss_b200_ctx* c, gss_b200_batch* b, gss_segment_diag* diags) {
   CU_TRY(c, cudaSetDevice(c->device));
   if (!b->ran) return fail(c, GSS_INTERNAL_ERROR, "batch_fetch before batch_run");
+  NvtxRange nv(c, "gss.d2h");
   cudaStream_t st = c->stream;
   const int F = b->cfg.stft.fft_size / 2 + 1;
   const int I = b->cfg.bss_iterations;
@@ -1143,11 +1200,11 @@ gss_status gss_b200_batch_fetch(gss_b200_ctx* c, gss_b200_batch* b, gss_segment_
     s.ref.resize(g.nseg);
     s.zeroed.resize(g.nseg);
     s.ll.resize(g.nseg);
-    CU_TRY(c, cudaMemcpyAsync(s.status.data(), g.status, sizeof(status_t) * g.nseg, cudaMemcpyDeviceToHost, st));
-    CU_TRY(c, cudaMemcpyAsync(s.ref.data(), g.ref, sizeof(int) * g.nseg, cudaMemcpyDeviceToHost, st));
-    CU_TRY(c, cudaMemcpyAsync(s.zeroed.data(), g.zeroed, sizeof(int) * g.nseg, cudaMemcpyDeviceToHost, st));
+    CU_TRY(c, cudaMemcpyAsync(s.status.data(), g.status, sizeof(status_t) * g.nseg, cudaMemcpyDefault, st));
+    CU_TRY(c, cudaMemcpyAsync(s.ref.data(), g.ref, sizeof(int) * g.nseg, cudaMemcpyDefault, st));
+    CU_TRY(c, cudaMemcpyAsync(s.zeroed.data(), g.zeroed, sizeof(int) * g.nseg, cudaMemcpyDefault, st));
     CU_TRY(c, cudaMemcpyAsync(s.ll.data(), g.seg_ll + (long long)I * g.nseg, sizeof(double) * g.nseg,
-                              cudaMemcpyDeviceToHost, st));
+                              cudaMemcpyDefault, st));
   }
   CU_TRY(c, cudaStreamSynchronize(st));
   for (size_t gi = 0; gi < b->groups.size(); ++gi) {
@@ -1176,19 +1233,19 @@ gss_status gss_b200_batch_fetch(gss_b200_ctx* c, gss_b200_batch* b, gss_segment_
         const int64_t len = hi - b->pb[i][p];
         if (len > 0)
           CU_TRY(c, cudaMemcpyAsync(d.out_wave + off, g.wave + sd.wave_off + b->pb[i][p], sizeof(float) * len,
-                                    cudaMemcpyDeviceToHost, st));
+                                    cudaMemcpyDefault, st));
         d.out_lengths[p] = len;
         off += len;
       }
       if (d.mono_out)
         CU_TRY(c, cudaMemcpyAsync(d.mono_out, g.wave + sd.wave_off, sizeof(float) * d.num_samples,
-                                  cudaMemcpyDeviceToHost, st));
+                                  cudaMemcpyDefault, st));
       if (d.gamma_out && sd.g_off >= 0)
         CU_TRY(c, cudaMemcpyAsync(d.gamma_out, g.gamma + sd.g_off, sizeof(float) * (size_t)F * sd.T * sd.K,
-                                  cudaMemcpyDeviceToHost, st));
+                                  cudaMemcpyDefault, st));
       if (d.h_out)
         CU_TRY(c, cudaMemcpyAsync(d.h_out, g.h + sd.f_off * g.M, sizeof(cdbl) * (size_t)F * g.M,
-                                  cudaMemcpyDeviceToHost, st));
+                                  cudaMemcpyDefault, st));
     }
   }
   cudaEventRecord(d2h1, st);
@@ -1235,6 +1292,7 @@ void gss_b200_batch_free(gss_b200_ctx* c, gss_b200_batch* b) {
 gss_status gss_b200_enhance_batch(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
                                   const gss_pipeline_config* cfg, gss_segment_diag* diags) {
   gss_b200_batch* b = nullptr;
+  NvtxRange nv(c, "gss.enhance_batch");
   // the audio goes up wave by wave from inside the run, each wave behind the previous wave's launches
   static const bool trace = std::getenv("GSS_B200_TRACE") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
@@ -1283,7 +1341,7 @@ gss_status check_tensor(gss_b200_ctx* c, int bins, int64_t frames, int channels)
 
 gss_status device_status(gss_b200_ctx* c, Group& g) {
   status_t s = kStatusOk;
-  CU_TRY(c, cudaMemcpyAsync(&s, g.status, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(&s, g.status, sizeof(s), cudaMemcpyDefault, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   if (s == kStatusOk) return GSS_OK;
   const int code = (int)(s >> 32);
@@ -1323,7 +1381,7 @@ gss_status gss_b200_stft(gss_b200_ctx* c, const float* audio, int32_t M, int64_t
   need.audio = need.y = true;
   rc = build_group(c, sg.g, M, 1, F, {s}, need, nullptr, 0);
   if (rc != GSS_OK) return rc;
-  CU_TRY(c, cudaMemcpyAsync(sg.g.audio, audio, sizeof(float) * (size_t)M * N, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(sg.g.audio, audio, sizeof(float) * (size_t)M * N, cudaMemcpyDefault, c->stream));
   StftArgs a;
   a.audio = sg.g.audio;
   a.y = sg.g.Y;
@@ -1338,8 +1396,8 @@ gss_status gss_b200_stft(gss_b200_ctx* c, const float* audio, int32_t M, int64_t
     KClock k(c, kK_stft);
     CU_TRY(c, launch_stft(a, 1, (int)T, c->stream));
   }
-  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Y, sizeof(float2) * (size_t)F * T * M, cudaMemcpyDeviceToHost, c->stream));
-  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Y, sizeof(float2) * (size_t)F * T * M, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, finish_call(c));
   return GSS_OK;
 }
 
@@ -1369,13 +1427,13 @@ gss_status gss_b200_istft(gss_b200_ctx* c, const float* spec, int32_t bins, int6
   rc = build_group(c, sg.g, M, 1, F, {s}, need, nullptr, 0);
   if (rc != GSS_OK) return rc;
   Group& g = sg.g;
-  CU_TRY(c, cudaMemcpyAsync(g.Y, spec, sizeof(float2) * (size_t)F * T * M, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.Y, spec, sizeof(float2) * (size_t)F * T * M, cudaMemcpyDefault, c->stream));
   std::vector<float2> sel((size_t)F * M);
   for (int ch = 0; ch < M; ++ch) {
     // channel selection through the beamformer kernel: h = e_ch
     for (int f = 0; f < F; ++f)
       for (int m = 0; m < M; ++m) sel[(size_t)f * M + m] = make_float2(m == ch ? 1.f : 0.f, 0.f);
-    CU_TRY(c, cudaMemcpyAsync(g.hconj, sel.data(), sizeof(float2) * sel.size(), cudaMemcpyHostToDevice, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(g.hconj, sel.data(), sizeof(float2) * sel.size(), cudaMemcpyDefault, c->stream));
     ApplyArgs aa;
     aa.y = g.Y;
     aa.hconj = g.hconj;
@@ -1400,9 +1458,9 @@ gss_status gss_b200_istft(gss_b200_ctx* c, const float* spec, int32_t bins, int6
       KClock k(c, kK_istft);
       CU_TRY(c, launch_istft(ia, 1, out_len, c->stream));
     }
-    CU_TRY(c, cudaMemcpyAsync(out + (size_t)ch * out_len, g.wave, sizeof(float) * out_len, cudaMemcpyDeviceToHost,
+    CU_TRY(c, cudaMemcpyAsync(out + (size_t)ch * out_len, g.wave, sizeof(float) * out_len, cudaMemcpyDefault,
                               c->stream));
-    CU_TRY(c, cudaStreamSynchronize(c->stream));
+    CU_TRY(c, finish_call(c));
   }
   return GSS_OK;
 }
@@ -1426,13 +1484,13 @@ gss_status gss_b200_wpe(gss_b200_ctx* c, const float* in, int32_t bins, int64_t 
   need.y = need.yd = need.wpe = true;
   rc = build_group(c, sg.g, M, 1, bins, {s}, need, cfg, 0);
   if (rc != GSS_OK) return rc;
-  CU_TRY(c, cudaMemcpyAsync(sg.g.Y, in, bytes, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(sg.g.Y, in, bytes, cudaMemcpyDefault, c->stream));
   rc = run_wpe(c, sg.g, *cfg);
   if (rc != GSS_OK) return rc;
   rc = device_status(c, sg.g);
   if (rc != GSS_OK) return rc;
-  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Yd, bytes, cudaMemcpyDeviceToHost, c->stream));
-  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Yd, bytes, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, finish_call(c));
   return GSS_OK;
 }
 
@@ -1454,7 +1512,7 @@ gss_status gss_b200_debug_wpe_gram(gss_b200_ctx* c, const float* in, int32_t bin
   const size_t per = (size_t)km * km + (size_t)km * M;
   cdbl* d_rp = g.mem.get<cdbl>(per * bins);
   if (!d_rp) return fail(c, GSS_CUDA_ERROR, "alloc");
-  CU_TRY(c, cudaMemcpyAsync(g.Y, in, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.Y, in, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyDefault, c->stream));
   WpeArgs a;
   a.yobs = g.Y;
   a.ycur = g.Y;
@@ -1481,7 +1539,7 @@ gss_status gss_b200_debug_wpe_gram(gss_b200_ctx* c, const float* in, int32_t bin
     KClock k(c, kK_wpe_power + step);
     CU_TRY(c, launch_wpe_step(step, a, 1, bins, (int)T, g.max_wchunks, c->stream));
   }
-  CU_TRY(c, cudaMemcpyAsync(out_rp, d_rp, sizeof(cdbl) * per * bins, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(out_rp, d_rp, sizeof(cdbl) * per * bins, cudaMemcpyDefault, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   return GSS_OK;
 }
@@ -1499,13 +1557,13 @@ gss_status gss_b200_unit_normalize(gss_b200_ctx* c, const float* in, int32_t bin
   rc = build_group(c, sg.g, M, 1, bins, {s}, need, nullptr, 0);
   if (rc != GSS_OK) return rc;
   const size_t bytes = sizeof(float2) * (size_t)bins * T * M;
-  CU_TRY(c, cudaMemcpyAsync(sg.g.Y, in, bytes, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(sg.g.Y, in, bytes, cudaMemcpyDefault, c->stream));
   {
     KClock k(c, kK_misc);
     CU_TRY(c, launch_unit_normalize(sg.g.Y, sg.g.Yd, (long long)bins * T, M, c->stream));
   }
-  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Yd, bytes, cudaMemcpyDeviceToHost, c->stream));
-  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  CU_TRY(c, cudaMemcpyAsync(out, sg.g.Yd, bytes, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, finish_call(c));
   return GSS_OK;
 }
 
@@ -1534,7 +1592,7 @@ static gss_status em_common(gss_b200_ctx* c, const float* yn, int32_t bins, int6
   if (rc != GSS_OK) return rc;
   Group& g = sg.g;
   const int KT = g.KT, MM = M * M;
-  CU_TRY(c, cudaMemcpyAsync(g.Y, yn, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.Y, yn, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyDefault, c->stream));
   std::vector<double> h_pi;
   std::vector<cdbl> h_b;
   if (from_state) {
@@ -1547,8 +1605,8 @@ static gss_status em_common(gss_b200_ctx* c, const float* yn, int32_t bins, int6
           h_b[((size_t)f * KT + k) * MM + i] = cd_make(shapes_in[2 * (((size_t)f * K + k) * MM + i)],
                                                         shapes_in[2 * (((size_t)f * K + k) * MM + i) + 1]);
       }
-    CU_TRY(c, cudaMemcpyAsync(g.pi, h_pi.data(), sizeof(double) * h_pi.size(), cudaMemcpyHostToDevice, c->stream));
-    CU_TRY(c, cudaMemcpyAsync(g.bstate, h_b.data(), sizeof(cdbl) * h_b.size(), cudaMemcpyHostToDevice, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(g.pi, h_pi.data(), sizeof(double) * h_pi.size(), cudaMemcpyDefault, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(g.bstate, h_b.data(), sizeof(cdbl) * h_b.size(), cudaMemcpyDefault, c->stream));
   }
   EmRun r{g.Y, 0, false, from_state, true};
   rc = run_em(c, g, r);
@@ -1557,13 +1615,13 @@ static gss_status em_common(gss_b200_ctx* c, const float* yn, int32_t bins, int6
   if (rc != GSS_OK) return rc;
   const int I = g.iterations;
   if (gamma)
-    CU_TRY(c, cudaMemcpyAsync(gamma, g.gamma, sizeof(float) * (size_t)bins * T * K, cudaMemcpyDeviceToHost, c->stream));
-  if (trace) CU_TRY(c, cudaMemcpyAsync(trace, g.seg_ll, sizeof(double) * (I + 1), cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(gamma, g.gamma, sizeof(float) * (size_t)bins * T * K, cudaMemcpyDefault, c->stream));
+  if (trace) CU_TRY(c, cudaMemcpyAsync(trace, g.seg_ll, sizeof(double) * (I + 1), cudaMemcpyDefault, c->stream));
   if (pi || shapes) {
     h_pi.resize((size_t)bins * KT);
     h_b.resize((size_t)bins * KT * MM);
-    CU_TRY(c, cudaMemcpyAsync(h_pi.data(), g.pi, sizeof(double) * h_pi.size(), cudaMemcpyDeviceToHost, c->stream));
-    CU_TRY(c, cudaMemcpyAsync(h_b.data(), g.bstate, sizeof(cdbl) * h_b.size(), cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(h_pi.data(), g.pi, sizeof(double) * h_pi.size(), cudaMemcpyDefault, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(h_b.data(), g.bstate, sizeof(cdbl) * h_b.size(), cudaMemcpyDefault, c->stream));
   }
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   if (pi || shapes)
@@ -1608,8 +1666,8 @@ gss_status gss_b200_mvdr_stats(gss_b200_ctx* c, const float* y, const float* gam
   rc = build_group(c, sg.g, M, K, bins, {s}, need, nullptr, 0);
   if (rc != GSS_OK) return rc;
   Group& g = sg.g;
-  CU_TRY(c, cudaMemcpyAsync(g.Y, y, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyHostToDevice, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(g.gamma, gamma, sizeof(float) * (size_t)bins * T * K, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.Y, y, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.gamma, gamma, sizeof(float) * (size_t)bins * T * K, cudaMemcpyDefault, c->stream));
   StatsPassArgs sp;
   sp.y = g.Y;
   sp.gamma = g.gamma;
@@ -1634,9 +1692,9 @@ gss_status gss_b200_mvdr_stats(gss_b200_ctx* c, const float* y, const float* gam
     CU_TRY(c, launch_mvdr_stats_final(EmShape{g.M, g.KT}, sf, 1, c->stream));
   }
   std::vector<double> tm(bins);
-  CU_TRY(c, cudaMemcpyAsync(tm.data(), g.tmass, sizeof(double) * bins, cudaMemcpyDeviceToHost, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(tgt, g.phi_t, sizeof(cdbl) * (size_t)bins * M * M, cudaMemcpyDeviceToHost, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(bg, g.phi_b, sizeof(cdbl) * (size_t)bins * M * M, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(tm.data(), g.tmass, sizeof(double) * bins, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(tgt, g.phi_t, sizeof(cdbl) * (size_t)bins * M * M, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(bg, g.phi_b, sizeof(cdbl) * (size_t)bins * M * M, cudaMemcpyDefault, c->stream));
   CU_TRY(c, cudaStreamSynchronize(c->stream));
   double total = 0.0;
   for (double v : tm) total += v;
@@ -1658,16 +1716,16 @@ static gss_status mvdr_common(gss_b200_ctx* c, const double* tgt, const double* 
   if (rc != GSS_OK) return rc;
   Group& g = sg.g;
   const size_t mb = sizeof(cdbl) * (size_t)bins * M * M;
-  CU_TRY(c, cudaMemcpyAsync(g.phi_t, tgt, mb, cudaMemcpyHostToDevice, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(g.phi_b, bg, mb, cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.phi_t, tgt, mb, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.phi_b, bg, mb, cudaMemcpyDefault, c->stream));
   if (h) {
     rc = run_mvdr_design(c, g, fixed_ref, false);
     if (rc != GSS_OK) return rc;
     rc = device_status(c, g);
     if (rc != GSS_OK) return rc;
     int z = 0;
-    CU_TRY(c, cudaMemcpyAsync(h, g.h, sizeof(cdbl) * (size_t)bins * M, cudaMemcpyDeviceToHost, c->stream));
-    CU_TRY(c, cudaMemcpyAsync(&z, g.zeroed, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(h, g.h, sizeof(cdbl) * (size_t)bins * M, cudaMemcpyDefault, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(&z, g.zeroed, sizeof(int), cudaMemcpyDefault, c->stream));
     CU_TRY(c, cudaStreamSynchronize(c->stream));
     if (zeroed) *zeroed = z;
   } else {
@@ -1689,7 +1747,7 @@ static gss_status mvdr_common(gss_b200_ctx* c, const double* tgt, const double* 
       CU_TRY(c, launch_select_reference(a, 1, c->stream));
     }
     int r = 0;
-    CU_TRY(c, cudaMemcpyAsync(&r, g.ref, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU_TRY(c, cudaMemcpyAsync(&r, g.ref, sizeof(int), cudaMemcpyDefault, c->stream));
     CU_TRY(c, cudaStreamSynchronize(c->stream));
     *ref_out = r;
   }
@@ -1723,8 +1781,8 @@ gss_status gss_b200_apply(gss_b200_ctx* c, const double* h, int32_t h_bins, int3
   Group& g = sg.g;
   std::vector<float2> hc((size_t)bins * M);
   for (size_t i = 0; i < hc.size(); ++i) hc[i] = make_float2((float)h[2 * i], -(float)h[2 * i + 1]);
-  CU_TRY(c, cudaMemcpyAsync(g.Y, y, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyHostToDevice, c->stream));
-  CU_TRY(c, cudaMemcpyAsync(g.hconj, hc.data(), sizeof(float2) * hc.size(), cudaMemcpyHostToDevice, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.Y, y, sizeof(float2) * (size_t)bins * T * M, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, cudaMemcpyAsync(g.hconj, hc.data(), sizeof(float2) * hc.size(), cudaMemcpyDefault, c->stream));
   ApplyArgs aa;
   aa.y = g.Y;
   aa.hconj = g.hconj;
@@ -1737,9 +1795,52 @@ gss_status gss_b200_apply(gss_b200_ctx* c, const double* h, int32_t h_bins, int3
     KClock k(c, kK_apply);
     CU_TRY(c, launch_apply(aa, 1, (int)T, c->stream));
   }
-  CU_TRY(c, cudaMemcpyAsync(out, g.X, sizeof(float2) * (size_t)bins * T, cudaMemcpyDeviceToHost, c->stream));
-  CU_TRY(c, cudaStreamSynchronize(c->stream));
+  CU_TRY(c, cudaMemcpyAsync(out, g.X, sizeof(float2) * (size_t)bins * T, cudaMemcpyDefault, c->stream));
+  CU_TRY(c, finish_call(c));
   return GSS_OK;
 }
+
+
+// ---- device-pointer variants: the same operators for callers whose tensors already live in HBM.
+// Tensor arguments are DEVICE pointers on the context's device; `stream` is the caller's CUDA stream (0 = the
+// legacy default stream): the call is ordered after the work already queued on it, and the stream waits for the
+// call's results, so the caller never synchronises with the host. Copies are device-to-device.
+gss_status gss_b200_stft_dev(gss_b200_ctx* c, const float* audio, int32_t M, int64_t N, int32_t signal_rate,
+                             const gss_stft_config* cfg, float* out, void* stream) {
+  DevCall scope(c, stream);
+  return gss_b200_stft(c, audio, M, N, signal_rate, cfg, out);
+}
+
+gss_status gss_b200_istft_dev(gss_b200_ctx* c, const float* spec, int32_t bins, int64_t T, int32_t M,
+                              int64_t num_samples, const gss_stft_config* cfg, float* out, void* stream) {
+  DevCall scope(c, stream);
+  return gss_b200_istft(c, spec, bins, T, M, num_samples, cfg, out);
+}
+
+gss_status gss_b200_wpe_dev(gss_b200_ctx* c, const float* in, int32_t bins, int64_t T, int32_t M,
+                            const gss_wpe_config* cfg, float* out, void* stream) {
+  DevCall scope(c, stream);
+  return gss_b200_wpe(c, in, bins, T, M, cfg, out);  // reads the device status word: one host wait, as a solve can fail
+}
+
+gss_status gss_b200_unit_normalize_dev(gss_b200_ctx* c, const float* in, int32_t bins, int64_t T, int32_t M,
+                                       float* out, void* stream) {
+  DevCall scope(c, stream);
+  return gss_b200_unit_normalize(c, in, bins, T, M, out);
+}
+
+gss_status gss_b200_apply_dev(gss_b200_ctx* c, const double* h, int32_t h_bins, int32_t h_channels, const float* y,
+                              int32_t bins, int64_t T, int32_t M, float* out, void* stream) {
+  DevCall scope(c, stream);
+  return gss_b200_apply(c, h, h_bins, h_channels, y, bins, T, M, out);  // h (F x M cdouble) stays a HOST array
+}
+
+gss_status gss_b200_enhance_batch_dev(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
+                                      const gss_pipeline_config* cfg, gss_segment_diag* diags, void* stream) {
+  DevCall scope(c, stream);
+  return gss_b200_enhance_batch(c, n, segs, cfg, diags);
+}
+
+int64_t gss_b200_nvtx_range_count(const gss_b200_ctx* c) { return c ? c->nvtx_ranges : 0; }
 
 }  // extern "C"

@@ -5,15 +5,20 @@
 // flat objects the manifests use (gss::manifests::detail::Json).
 #pragma once
 
+#include <algorithm>
 #include <cctype>
+#include <cerrno>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
 #include <map>
+#include <memory>
 #include <set>
 #include <sstream>
 #include <string>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #ifdef GSS_WITH_ZLIB
@@ -114,52 +119,79 @@ inline ActivityMatrix build_activity(const std::vector<Segment>& segments, int64
 }
 
 // ---------------------------------------------------------------------------
-// file reading (gzip-transparent by extension), manifests.hpp:79-114
+// Text files. A name ending in ".gz" goes through zlib (when built with -DGSS_WITH_ZLIB), anything else through
+// stdio; callers never see the difference (the reference's read_text / write_text contract, manifests.hpp:79-114).
 // ---------------------------------------------------------------------------
 inline bool has_suffix(const std::string& s, const std::string& suffix) {
-  return s.size() >= suffix.size() && s.compare(s.size() - suffix.size(), suffix.size(), suffix) == 0;
+  const size_t n = suffix.size();
+  return s.size() >= n && std::equal(suffix.begin(), suffix.end(), s.end() - static_cast<std::ptrdiff_t>(n));
 }
 
-inline std::string read_text(const std::string& path) {
-  if (has_suffix(path, ".gz")) {
+namespace textio {
+
+constexpr size_t kBlock = 1u << 16;
+
 #ifdef GSS_WITH_ZLIB
-    gzFile gz = gzopen(path.c_str(), "rb");
-    if (!gz) throw IoError("cannot open file: " + path);
-    std::string out;
-    char buf[1 << 16];
-    int n;
-    while ((n = gzread(gz, buf, sizeof buf)) > 0) out.append(buf, n);
-    gzclose(gz);
-    if (n < 0) throw IoError("gzip read failed: " + path);
-    return out;
-#else
-    throw IoError("built without zlib (GSS_WITH_ZLIB): cannot read " + path);
-#endif
+struct GzClose {
+  void operator()(gzFile_s* g) const {
+    if (g) gzclose(g);
   }
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw IoError("cannot open file: " + path);
-  std::ostringstream ss;
-  ss << in.rdbuf();
-  return ss.str();
+};
+using Gz = std::unique_ptr<gzFile_s, GzClose>;
+#endif
+
+struct FileClose {
+  void operator()(std::FILE* f) const {
+    if (f) std::fclose(f);
+  }
+};
+using Plain = std::unique_ptr<std::FILE, FileClose>;
+
+}  // namespace textio
+
+inline std::string read_text(const std::string& path) {
+  std::string text;
+  std::vector<char> block(textio::kBlock);
+  if (!has_suffix(path, ".gz")) {
+    textio::Plain f(std::fopen(path.c_str(), "rb"));
+    if (!f) throw IoError("cannot open file: " + path);
+    for (size_t got; (got = std::fread(block.data(), 1, block.size(), f.get())) > 0;) text.append(block.data(), got);
+    if (std::ferror(f.get())) throw IoError("read failed: " + path);
+    return text;
+  }
+#ifdef GSS_WITH_ZLIB
+  textio::Gz g(gzopen(path.c_str(), "rb"));
+  if (!g) throw IoError("cannot open file: " + path);
+  int got = 0;
+  while ((got = gzread(g.get(), block.data(), static_cast<unsigned>(block.size()))) > 0)
+    text.append(block.data(), static_cast<size_t>(got));
+  if (got < 0) throw IoError("gzip stream is damaged: " + path);
+  return text;
+#else
+  throw IoError("this build has no zlib (GSS_WITH_ZLIB), cannot read " + path);
+#endif
 }
 
 inline void write_text(const std::string& path, const std::string& content) {
-  if (has_suffix(path, ".gz")) {
-#ifdef GSS_WITH_ZLIB
-    gzFile gz = gzopen(path.c_str(), "wb");
-    if (!gz) throw IoError("cannot create file: " + path);
-    const int n = gzwrite(gz, content.data(), static_cast<unsigned>(content.size()));
-    gzclose(gz);
-    if (n != static_cast<int>(content.size())) throw IoError("gzip write failed: " + path);
+  if (!has_suffix(path, ".gz")) {
+    textio::Plain f(std::fopen(path.c_str(), "wb"));
+    if (!f) throw IoError("cannot create file: " + path);
+    const bool ok = std::fwrite(content.data(), 1, content.size(), f.get()) == content.size();
+    if (!ok || std::fflush(f.get()) != 0) throw IoError("write failed: " + path);
     return;
-#else
-    throw IoError("built without zlib (GSS_WITH_ZLIB): cannot write " + path);
-#endif
   }
-  std::ofstream os(path, std::ios::binary | std::ios::trunc);
-  if (!os) throw IoError("cannot create file: " + path);
-  os << content;
-  if (!os) throw IoError("write failed: " + path);
+#ifdef GSS_WITH_ZLIB
+  textio::Gz g(gzopen(path.c_str(), "wb"));
+  if (!g) throw IoError("cannot create file: " + path);
+  for (size_t at = 0; at < content.size();) {
+    const unsigned want = static_cast<unsigned>(std::min(textio::kBlock, content.size() - at));
+    if (gzwrite(g.get(), content.data() + at, want) != static_cast<int>(want)) throw IoError("gzip write failed: " + path);
+    at += want;
+  }
+  if (gzclose(g.release()) != Z_OK) throw IoError("gzip write failed: " + path);
+#else
+  throw IoError("this build has no zlib (GSS_WITH_ZLIB), cannot write " + path);
+#endif
 }
 
 namespace detail {
@@ -458,114 +490,160 @@ inline void save_segments(const std::string& path, const std::vector<Segment>& s
   write_text(path, serialize_segments(segs));
 }
 
-/// Segments of a JSONL or RTTM manifest; entries with duration <= 0 are dropped and counted in *skipped.
-inline std::vector<Segment> load_segments(const std::string& path, SegmentFormat format = SegmentFormat::kJsonl,
-                                          int* skipped = nullptr) {
-  if (skipped) *skipped = 0;
-  std::vector<Segment> out;
-  if (format == SegmentFormat::kJsonl) {
-    detail::for_each_jsonl(path, [&](const detail::Json& j, long) {
-      Segment s;
-      s.id = j.at("id").as_string();
-      s.recording_id = j.at("recording_id").as_string();
-      s.speaker = j.at("speaker").as_string();
-      s.start = j.at("start").as_number();
-      s.duration = j.at("duration").as_number();
-      if (s.duration <= 0.0) {  // the reference warns and drops the entry
-        if (skipped) ++*skipped;
-        return;
-      }
-      out.push_back(std::move(s));
-    });
-    return out;
-  }
-  std::istringstream in(read_text(path));
-  std::string line;
-  long line_no = 0;
-  std::map<std::pair<std::string, std::string>, int> counters;
-  while (std::getline(in, line)) {
-    ++line_no;
-    std::istringstream ls(line);
-    std::vector<std::string> fields;
-    for (std::string tok; ls >> tok;) fields.push_back(tok);
-    if (fields.empty() || fields[0] != "SPEAKER") continue;  // other record types are legal
-    if (fields.size() < 9)
-      throw ParseError(detail::loc(path, line_no) + "RTTM SPEAKER line has " + std::to_string(fields.size()) +
-                       " fields, need 9+");
-    Segment s;
-    s.recording_id = fields[1];
-    s.speaker = fields[7];
-    try {
-      size_t used = 0;
-      s.start = std::stod(fields[3], &used);
-      if (used != fields[3].size()) throw std::invalid_argument(fields[3]);
-      s.duration = std::stod(fields[4], &used);
-      if (used != fields[4].size()) throw std::invalid_argument(fields[4]);
-    } catch (const std::exception&) {
-      throw ParseError(detail::loc(path, line_no) + "RTTM line has non-numeric start/duration");
-    }
-    if (s.duration <= 0.0) {
-      if (skipped) ++*skipped;
-      continue;
-    }
-    const int n = counters[{s.recording_id, s.speaker}]++;
-    char idx[16];
-    std::snprintf(idx, sizeof idx, "%04d", n);
-    s.id = s.recording_id + "-" + s.speaker + "-" + idx;
-    out.push_back(std::move(s));
+namespace detail {
+
+/// Whitespace-separated fields of one text line (RTTM is a column format).
+inline std::vector<std::string> split_fields(const std::string& line) {
+  std::vector<std::string> out;
+  size_t i = 0;
+  const size_t n = line.size();
+  while (i < n) {
+    while (i < n && std::isspace(static_cast<unsigned char>(line[i]))) ++i;
+    size_t j = i;
+    while (j < n && !std::isspace(static_cast<unsigned char>(line[j]))) ++j;
+    if (j > i) out.emplace_back(line, i, j - i);
+    i = j;
   }
   return out;
 }
 
-/// Cross-manifest validation; human-readable problems (empty = OK), manifests.hpp:334-361.
-inline std::vector<std::string> validate(const std::vector<Recording>& recordings, const std::vector<Segment>& segments) {
-  std::vector<std::string> problems;
-  std::map<std::string, const Recording*> by_id;
-  for (const auto& r : recordings) by_id[r.id] = &r;
-  std::set<std::string> seg_ids;
-  for (const auto& s : segments) {
-    if (!seg_ids.insert(s.id).second) problems.push_back("duplicate segment id '" + s.id + "'");
-    const auto it = by_id.find(s.recording_id);
-    if (it == by_id.end()) {
-      problems.push_back("segment '" + s.id + "' references unknown recording '" + s.recording_id + "'");
-      continue;
-    }
-    if (s.start < 0.0) problems.push_back("segment '" + s.id + "' starts at " + detail::json_number(s.start));
-    if (s.end() > it->second->duration + 1e-6)
-      problems.push_back("segment '" + s.id + "' ends at " + detail::json_number(s.end()) + ", past recording end " +
-                         detail::json_number(it->second->duration));
-  }
-  return problems;
+/// The whole token as a double, or false.
+inline bool whole_number(const std::string& tok, double& value) {
+  if (tok.empty()) return false;
+  char* end = nullptr;
+  errno = 0;
+  value = std::strtod(tok.c_str(), &end);
+  return errno == 0 && end == tok.c_str() + tok.size();
 }
 
-/// [start_sample, start_sample + count) across all sources of a recording, channels stacked in source order;
-/// channel_subset selects stacked indices (empty = all). manifests.hpp:442-479.
-inline stft::RealSignal load_audio(const Recording& rec, int64_t start_sample, int64_t count,
-                                   const std::vector<int>& channel_subset = {}) {
-  stft::RealSignal all;
-  all.sample_rate = rec.sample_rate;
-  for (const auto& src : rec.sources) {
-    stft::RealSignal part = wav::read(src.path, start_sample, count);
-    if (part.sample_rate != rec.sample_rate)
-      throw ConfigError("recording '" + rec.id + "': " + src.path + " is " + std::to_string(part.sample_rate) +
-                        " Hz, manifest says " + std::to_string(rec.sample_rate));
-    if (part.num_samples() < count)
-      throw IoError("recording '" + rec.id + "': " + src.path + " has " + std::to_string(part.num_samples()) +
-                    " samples at offset " + std::to_string(start_sample) + ", need " + std::to_string(count));
-    for (const int c : src.channels) {
-      if (c < 0 || c >= part.num_channels())
-        throw ConfigError("recording '" + rec.id + "': " + src.path + " has no channel " + std::to_string(c));
-      all.channels.push_back(std::move(part.channels[c]));
+/// RTTM: "SPEAKER <recording> <chan> <start> <duration> <NA> <NA> <speaker> <NA> ..." (manifests.hpp:274-318);
+/// other record types are skipped, ids are made up as <recording>-<speaker>-<running number per pair>.
+inline void parse_rttm(const std::string& path, std::vector<Segment>& out, int& dropped) {
+  const std::string text = read_text(path);
+  std::map<std::string, int> next_index;  // key: recording + '\n' + speaker
+  long line_no = 0;
+  for (size_t at = 0; at < text.size();) {
+    size_t eol = text.find('\n', at);
+    if (eol == std::string::npos) eol = text.size();
+    const std::vector<std::string> col = split_fields(text.substr(at, eol - at));
+    at = eol + 1;
+    ++line_no;
+    if (col.empty() || col.front() != "SPEAKER") continue;
+    if (col.size() < 9)
+      throw ParseError(loc(path, line_no) + "RTTM SPEAKER line has " + std::to_string(col.size()) + " fields, need 9+");
+    Segment seg;
+    if (!whole_number(col[3], seg.start) || !whole_number(col[4], seg.duration))
+      throw ParseError(loc(path, line_no) + "RTTM line has non-numeric start/duration");
+    if (!(seg.duration > 0.0)) {
+      ++dropped;
+      continue;
+    }
+    seg.recording_id = col[1];
+    seg.speaker = col[7];
+    int& n = next_index[seg.recording_id + '\n' + seg.speaker];
+    std::string number = std::to_string(n++);
+    if (number.size() < 4) number.insert(0, 4 - number.size(), '0');
+    seg.id = seg.recording_id + "-" + seg.speaker + "-" + number;
+    out.push_back(std::move(seg));
+  }
+}
+
+inline void parse_segment_lines(const std::string& path, std::vector<Segment>& out, int& dropped) {
+  for_each_jsonl(path, [&](const Json& j, long) {
+    Segment seg;
+    seg.id = j.at("id").as_string();
+    seg.recording_id = j.at("recording_id").as_string();
+    seg.speaker = j.at("speaker").as_string();
+    seg.start = j.at("start").as_number();
+    seg.duration = j.at("duration").as_number();
+    if (seg.duration > 0.0)
+      out.push_back(std::move(seg));
+    else
+      ++dropped;  // the reference warns and drops the entry
+  });
+}
+
+}  // namespace detail
+
+/// Segments of a JSONL or RTTM manifest; entries with duration <= 0 are dropped and counted in *skipped
+/// (manifests.hpp:253-331).
+inline std::vector<Segment> load_segments(const std::string& path, SegmentFormat format = SegmentFormat::kJsonl,
+                                          int* skipped = nullptr) {
+  std::vector<Segment> out;
+  int dropped = 0;
+  if (format == SegmentFormat::kRttm)
+    detail::parse_rttm(path, out, dropped);
+  else
+    detail::parse_segment_lines(path, out, dropped);
+  if (skipped) *skipped = dropped;
+  return out;
+}
+
+/// Cross-manifest checks, one sentence per finding, empty when the manifests fit (manifests.hpp:334-361): segment
+/// ids unique, every segment inside a known recording.
+inline std::vector<std::string> validate(const std::vector<Recording>& recordings, const std::vector<Segment>& segments) {
+  std::unordered_map<std::string, double> length_of;
+  for (const Recording& r : recordings) length_of[r.id] = r.duration;
+  std::unordered_set<std::string> seen;
+  std::vector<std::string> findings;
+  auto say = [&findings](std::string text) { findings.push_back(std::move(text)); };
+  const double slack = 1e-6;  // seconds a segment may overhang its recording
+  for (const Segment& seg : segments) {
+    const std::string who = "segment '" + seg.id + "'";
+    if (seen.count(seg.id)) say("duplicate segment id '" + seg.id + "'");
+    seen.insert(seg.id);
+    const auto rec = length_of.find(seg.recording_id);
+    if (rec == length_of.end()) {
+      say(who + " references unknown recording '" + seg.recording_id + "'");
+    } else {
+      if (seg.start < 0.0) say(who + " starts at " + detail::json_number(seg.start));
+      if (seg.end() > rec->second + slack)
+        say(who + " ends at " + detail::json_number(seg.end()) + ", past recording end " + detail::json_number(rec->second));
     }
   }
-  if (channel_subset.empty()) return all;
+  return findings;
+}
+
+/// Samples [start_sample, start_sample + count) of a recording whose channels are spread over several files: the
+/// stacked channel list is the files' channel lists in manifest order, `channel_subset` picks from that list
+/// (empty = everything). Every file is opened once and only the picked channels are kept (manifests.hpp:442-479).
+inline stft::RealSignal load_audio(const Recording& rec, int64_t start_sample, int64_t count,
+                                   const std::vector<int>& channel_subset = {}) {
+  struct Pick {
+    size_t source;
+    int channel;
+  };
+  std::vector<Pick> stacked;
+  for (size_t i = 0; i < rec.sources.size(); ++i)
+    for (const int c : rec.sources[i].channels) stacked.push_back({i, c});
+  std::vector<Pick> wanted;
+  if (channel_subset.empty()) {
+    wanted = stacked;
+  } else {
+    for (const int k : channel_subset) {
+      if (k < 0 || k >= static_cast<int>(stacked.size()))
+        throw ConfigError("channel subset index " + std::to_string(k) + " out of range [0, " +
+                          std::to_string(stacked.size()) + ")");
+      wanted.push_back(stacked[static_cast<size_t>(k)]);
+    }
+  }
   stft::RealSignal out;
-  out.sample_rate = all.sample_rate;
-  for (const int c : channel_subset) {
-    if (c < 0 || c >= all.num_channels())
-      throw ConfigError("channel subset index " + std::to_string(c) + " out of range [0, " +
-                        std::to_string(all.num_channels()) + ")");
-    out.channels.push_back(all.channels[c]);
+  out.sample_rate = rec.sample_rate;
+  out.channels.resize(wanted.size());
+  for (size_t i = 0; i < rec.sources.size(); ++i) {
+    const Source& src = rec.sources[i];
+    const std::string where = "recording '" + rec.id + "': " + src.path;
+    stft::RealSignal file = wav::read(src.path, start_sample, count);
+    if (file.sample_rate != rec.sample_rate)
+      throw ConfigError(where + " is " + std::to_string(file.sample_rate) + " Hz, manifest says " +
+                        std::to_string(rec.sample_rate));
+    if (file.num_samples() < count)
+      throw IoError(where + " has " + std::to_string(file.num_samples()) + " samples at offset " +
+                    std::to_string(start_sample) + ", need " + std::to_string(count));
+    for (const int c : src.channels)
+      if (c < 0 || c >= file.num_channels()) throw ConfigError(where + " has no channel " + std::to_string(c));
+    for (size_t k = 0; k < wanted.size(); ++k)
+      if (wanted[k].source == i) out.channels[k] = file.channels[static_cast<size_t>(wanted[k].channel)];
   }
   return out;
 }

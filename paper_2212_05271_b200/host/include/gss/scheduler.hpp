@@ -26,6 +26,7 @@
 #include <string>
 #include <thread>
 #include <utility>
+#include <unordered_map>
 #include <vector>
 
 #include "beamform.hpp"
@@ -107,50 +108,58 @@ struct BatchPlan {
   }
 };
 
-/// Groups segments by (recording, speaker) in first-appearance order, fills batches greedily in temporal
-/// order up to the duration cap, then emits round-robin across groups; oversized segments stay singletons
-/// (scheduler.hpp:101-160).
+/// The batch plan (the reference's contract, scheduler.hpp:101-160): segments of one (recording, speaker) pair are
+/// packed in temporal order into batches of at most `max_batch_duration` seconds of speech; a segment longer than
+/// the cap is a batch of its own, and so is every segment in one-per-batch mode. Batches are emitted in rounds:
+/// first batch of every pair (pairs in order of first appearance), then the second of every pair, and so on.
 inline std::vector<BatchPlan> plan_batches(const std::vector<manifests::Segment>& segments, double max_batch_duration,
                                            BatchMode mode = BatchMode::kSuperSegment) {
-  using Key = std::pair<std::string, std::string>;
-  std::vector<Key> order;
-  std::map<Key, std::vector<manifests::Segment>> groups;
-  for (const auto& s : segments) {
-    const Key key{s.recording_id, s.speaker};
-    if (groups.find(key) == groups.end()) order.push_back(key);
-    groups[key].push_back(s);
-  }
-  std::vector<std::vector<BatchPlan>> per_group;
-  for (const Key& key : order) {
-    auto& segs = groups[key];
-    std::sort(segs.begin(), segs.end(), [](const manifests::Segment& a, const manifests::Segment& b) {
-      return a.start != b.start ? a.start < b.start : a.id < b.id;
-    });
-    std::vector<BatchPlan> buckets;
-    for (const auto& s : segs) {
-      const bool alone = mode == BatchMode::kOnePerBatch || s.duration > max_batch_duration ||
-                         (!buckets.empty() && buckets.back().parts.size() == 1 &&
-                          buckets.back().parts[0].duration > max_batch_duration);
-      if (alone) {
-        buckets.push_back(BatchPlan{key.first, key.second, {s}});
-        continue;
-      }
-      if (buckets.empty() || buckets.back().total_duration() + s.duration > max_batch_duration)
-        buckets.push_back(BatchPlan{key.first, key.second, {}});
-      buckets.back().parts.push_back(s);
+  // pair number of every segment, in order of first appearance
+  std::unordered_map<std::string, int> pair_of;
+  std::vector<int> pair(segments.size());
+  for (size_t i = 0; i < segments.size(); ++i)
+    pair[i] = pair_of.emplace(segments[i].recording_id + '\n' + segments[i].speaker, static_cast<int>(pair_of.size()))
+                  .first->second;
+  // one pass over the segments sorted by (pair, start, id)
+  std::vector<size_t> by_time(segments.size());
+  for (size_t i = 0; i < by_time.size(); ++i) by_time[i] = i;
+  std::sort(by_time.begin(), by_time.end(), [&](size_t x, size_t y) {
+    if (pair[x] != pair[y]) return pair[x] < pair[y];
+    if (segments[x].start != segments[y].start) return segments[x].start < segments[y].start;
+    return segments[x].id < segments[y].id;
+  });
+  struct Ranked {
+    int rank;  // position of the batch within its pair
+    int pair;
+    BatchPlan plan;
+  };
+  std::vector<Ranked> made;
+  int current = -1;
+  bool open = false;   // the last batch of `current` may still take segments
+  double filled = 0;
+  for (const size_t i : by_time) {
+    const manifests::Segment& seg = segments[i];
+    if (pair[i] != current) {
+      current = pair[i];
+      open = false;
     }
-    per_group.push_back(std::move(buckets));
+    const bool solitary = mode == BatchMode::kOnePerBatch || seg.duration > max_batch_duration;
+    if (solitary || !open || filled + seg.duration > max_batch_duration) {
+      const int rank = (!made.empty() && made.back().pair == current) ? made.back().rank + 1 : 0;
+      made.push_back(Ranked{rank, current, BatchPlan{seg.recording_id, seg.speaker, {}}});
+      filled = 0;
+      open = !solitary;
+    }
+    made.back().plan.parts.push_back(seg);
+    filled += seg.duration;
   }
+  std::stable_sort(made.begin(), made.end(), [](const Ranked& x, const Ranked& y) {
+    return x.rank != y.rank ? x.rank < y.rank : x.pair < y.pair;
+  });
   std::vector<BatchPlan> plans;
-  for (size_t round = 0;; ++round) {
-    bool any = false;
-    for (auto& buckets : per_group)
-      if (round < buckets.size()) {
-        plans.push_back(std::move(buckets[round]));
-        any = true;
-      }
-    if (!any) return plans;
-  }
+  plans.reserve(made.size());
+  for (Ranked& r : made) plans.push_back(std::move(r.plan));
+  return plans;
 }
 
 struct SuperSegment {  // scheduler.hpp:165-180
@@ -348,41 +357,50 @@ inline SuperSegment assemble(const BatchPlan& plan, const manifests::Recording& 
 // ---------------------------------------------------------------------------
 namespace detail {
 
-struct LoadedBatch {  // scheduler.hpp:371-376
+/// What a loader hands to the compute side: the assembled super-segment of plan entry `index`, or why it could
+/// not be assembled (the role of the reference's LoadedBatch, scheduler.hpp:371-376).
+struct LoadedBatch {
   int64_t index = 0;
   std::optional<SuperSegment> batch;  // empty on load failure
   std::string error;
   double load_seconds = 0.0;
 };
 
-/// Bounded queue that hands batches to the consumer in plan order whichever loader finished first
-/// (scheduler.hpp:383-412): this is what makes the worker count invisible in the output.
+/// Re-sequencer between the loader threads and the compute side. Loaders finish in any order; the consumer gets
+/// plan entries 0, 1, 2, ... . At most `capacity` entries ahead of the consumer are admitted, so a loader that
+/// runs far ahead waits instead of piling up audio in memory. This is what makes the worker count invisible in the
+/// output (the contract of the reference's OrderedBatchQueue, scheduler.hpp:383-412). Here: a ring of `capacity`
+/// slots addressed by index modulo capacity, one mutex, one condition variable.
 class OrderedBatchQueue {
  public:
-  explicit OrderedBatchQueue(int64_t capacity) : capacity_(capacity) {}
+  explicit OrderedBatchQueue(int64_t capacity) : ring_(static_cast<size_t>(capacity < 1 ? 1 : capacity)) {}
+
+  /// Blocks while item.index is `capacity` or more entries ahead of the consumer.
   void put(LoadedBatch&& item) {
-    std::unique_lock<std::mutex> lock(mu_);
-    const int64_t idx = item.index;
-    space_.wait(lock, [&] { return idx < next_ + capacity_; });
-    ready_.emplace(idx, std::move(item));
-    available_.notify_all();
+    const int64_t n = static_cast<int64_t>(ring_.size());
+    std::unique_lock<std::mutex> hold(lock_);
+    changed_.wait(hold, [&] { return item.index - head_ < n; });
+    ring_[static_cast<size_t>(item.index % n)] = std::move(item);
+    changed_.notify_all();
   }
+
+  /// Blocks until the next entry in plan order has arrived.
   LoadedBatch take() {
-    std::unique_lock<std::mutex> lock(mu_);
-    available_.wait(lock, [&] { return ready_.count(next_) > 0; });
-    LoadedBatch item = std::move(ready_.at(next_));
-    ready_.erase(next_);
-    ++next_;
-    space_.notify_all();
-    return item;
+    std::unique_lock<std::mutex> hold(lock_);
+    std::optional<LoadedBatch>& slot = ring_[static_cast<size_t>(head_ % static_cast<int64_t>(ring_.size()))];
+    changed_.wait(hold, [&] { return slot.has_value(); });
+    LoadedBatch out = std::move(*slot);
+    slot.reset();
+    ++head_;
+    changed_.notify_all();
+    return out;
   }
 
  private:
-  const int64_t capacity_;
-  std::mutex mu_;
-  std::condition_variable space_, available_;
-  std::map<int64_t, LoadedBatch> ready_;
-  int64_t next_ = 0;
+  std::vector<std::optional<LoadedBatch>> ring_;
+  std::mutex lock_;
+  std::condition_variable changed_;
+  int64_t head_ = 0;  // plan index the consumer takes next
 };
 
 inline double seconds_since(std::chrono::steady_clock::time_point t0) {
@@ -491,20 +509,18 @@ inline RunSummary run_pipeline(const std::vector<manifests::Recording>& recordin
   using manifests::detail::json_number;
   cfg.validate();
   const auto wall0 = std::chrono::steady_clock::now();
-  {
-    const auto problems = manifests::validate(recordings, segments);
-    if (!problems.empty()) {
-      std::string joined;
-      for (const auto& p : problems) joined += "\n  " + p;
-      throw ConfigError("manifest validation failed:" + joined);
-    }
+  if (const std::vector<std::string> findings = manifests::validate(recordings, segments); !findings.empty()) {
+    std::string report = "manifest validation failed:";
+    for (const std::string& line : findings) report.append("\n  ").append(line);
+    throw ConfigError(report);
   }
   std::filesystem::create_directories(cfg.out_dir);
-  std::map<std::string, const manifests::Recording*> rec_by_id;
-  for (const auto& r : recordings) rec_by_id[r.id] = &r;
+  std::unordered_map<std::string, const manifests::Recording*> rec_by_id;
+  rec_by_id.reserve(recordings.size());
+  for (const manifests::Recording& r : recordings) rec_by_id.emplace(r.id, &r);
   const std::vector<BatchPlan> plans = plan_batches(segments, cfg.max_batch_duration, cfg.mode);
-  if (devices.empty()) devices = {0};
-  gpu_batch = std::max(gpu_batch, 1);
+  if (devices.empty()) devices.push_back(0);
+  if (gpu_batch < 1) gpu_batch = 1;
 
   RunSummary run;
   run.num_batches = static_cast<int64_t>(plans.size());

@@ -57,8 +57,9 @@ def check_against_oracle(got, want, label="", max_abs=2e-2):
         assert sdr_db(a, b) >= 40.0
 
 
-CFG2_MAX_ABS = 2e-2  # placeholder until measured
-CFG4_MAX_ABS = 2e-2
+CFG2_MAX_ABS = 4e-3       # measured 1.8e-3 on B200 (segment 0)
+CFG4_MAX_ABS = 2e-2       # only used if the oracle is stable on every bin of the segment
+SWEEP_5_3_40_CAP = 0.50   # 40 iterations: measured below
 
 
 def test_enhance_tiny_batch_with_wpe(gss, oracle):
@@ -78,30 +79,23 @@ def test_enhance_cfg1_no_wpe(gss, oracle):
     check_against_oracle(r, oracle_enhance(oracle, w.segments[0], w.cfg), "cfg1", max_abs=8e-3)  # measured 3.9e-3
 
 
-def test_enhance_cfg2_the_librispeech_css_shape(gss, oracle):
-    # BASELINE configs[1]: 7 channels, 3 speakers + noise, WPE (taps 10, delay 2), 10 s + 2 x 15 s context, T = 5001
+def test_enhance_cfg2_the_libricss_shape(gss, oracle, simd_oracle):
+    # BASELINE configs[1]: 7 channels, 3 speakers + noise, WPE (taps 10, delay 2), 10 s + 2 x 15 s context, T = 5001.
+    # Segment 0 is stable on every bin (strict gates); segment 1 has a bin that 20 EM iterations flip for the oracle too
     import synthbench as synth
     w = synth.workload("cfg2", n_segments=2)
-    res = gss.scheduler.enhance_batches(w.segments, w.cfg, diagnostics=True)
-    for i, (ss, r) in enumerate(zip(w.segments, res)):
+    for i, ss in enumerate(w.segments):
+        r = check_segment(gss, oracle, simd_oracle, ss, w.cfg, f"cfg2[{i}]", max_abs=CFG2_MAX_ABS, max_unstable=0.02)
         assert r.frames == 5001 and len(r.outputs[0]) == 160000
-        check_against_oracle(r, oracle_enhance(oracle, ss, w.cfg), f"cfg2[{i}]", max_abs=CFG2_MAX_ABS)
 
 
-def test_enhance_cfg4_sixty_second_windows(gss, oracle):
+def test_enhance_cfg4_sixty_second_windows(gss, oracle, simd_oracle):
     # BASELINE configs[3]: 8 channels, 4 speakers + noise, 30 s segments + 2 x 15 s context: T = 7501 frames, all
     # 257 bins in one launch
     import synthbench as synth
     w = synth.workload("cfg4", n_segments=1)
-    ss, cfg = w.segments[0], w.cfg
-    r = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
+    r = check_segment(gss, oracle, simd_oracle, w.segments[0], w.cfg, "cfg4", max_abs=CFG4_MAX_ABS, max_unstable=0.02)
     assert r.frames == 7501 and len(r.outputs[0]) == 480000
-    want = oracle_enhance(oracle, ss, cfg)
-    unstable = oracle_unstable_bins(oracle, ss, cfg)
-    if unstable.any():  # as on cfg3: gate over the bins the oracle itself is stable on, and bound their number
-        check_on_stable_bins(r, want, unstable, "cfg4", 1e-3, max_unstable=0.02, cfg=cfg)
-    else:
-        check_against_oracle(r, want, "cfg4", max_abs=CFG4_MAX_ABS)
 
 
 def test_enhance_ragged_batch_mixed_shapes(gss, oracle):
@@ -228,16 +222,24 @@ def oracle_unstable_bins(oracle, ss, cfg, threshold=1e-2):
     return unstable
 
 
-def oracle_self_sdr(oracle, ss, cfg, want):
-    """SDR between the oracle's waveform and the oracle's waveform for the same audio multiplied by
-    (1 + 1e-7 N(0,1)): what "equal to the oracle" can mean for this segment. Far above 40 dB on well-conditioned
-    segments; it collapses when a strong bin is ill-conditioned for WPE (see oracle_unstable_bins)."""
-    import copy
-    rng = np.random.default_rng(1)
-    pert = copy.copy(ss)
-    pert.audio = type(ss.audio)((ss.audio.channels * (1.0 + 1e-7 * rng.standard_normal(ss.audio.channels.shape)))
-                                .astype(np.float32), ss.audio.sample_rate)
-    return sdr_db(oracle_enhance(oracle, pert, cfg).mono, want.mono)
+@pytest.fixture(scope="module")
+def simd_oracle(oracle, tmp_path_factory):
+    """Path of the oracle built with -DGSS_ORACLE_VECTOR_GRAM: the same arithmetic with another float summation
+    order inside a Gram chunk (what any second FP32 implementation of the reference, Eigen's GEMM included, is)."""
+    return oracle.build(out_dir=str(tmp_path_factory.mktemp("oracle_simd")), vector_gram=True)
+
+
+def oracle_order_noise(oracle, simd_oracle, ss, cfg, want, threshold=1e-2):
+    """(whole-waveform SDR, per-bin flags) between the oracle and its SIMD-Gram build on the same input: the level
+    at which "equal to the oracle" stops being defined for this segment. Above 95 dB on well-conditioned segments;
+    24 dB on a 2-channel segment whose DC bin is nearly rank-deficient for WPE (profiles/parity_r02.md)."""
+    try:
+        oracle.load(simd_oracle)
+        other = oracle_enhance(oracle, ss, cfg)
+    finally:
+        oracle.load(oracle._LIB_PATH)
+    dg = np.abs(other.gamma - want.gamma)
+    return sdr_db(other.mono, want.mono), dg.reshape(dg.shape[0], -1).max(axis=1) > threshold
 
 
 def banded_sdr_db(est, ref, keep, fft_size, shift):
@@ -251,10 +253,12 @@ def banded_sdr_db(est, ref, keep, fft_size, shift):
     return float(10 * np.log10(np.sum(np.abs(b) ** 2) / max(np.sum(np.abs(a - b) ** 2), 1e-300)))
 
 
-def check_on_stable_bins(got, want, unstable, label, ll_gate, max_unstable=0.02, cfg=None):
+def check_on_stable_bins(got, want, unstable, label, ll_gate, max_unstable=0.02, cfg=None, order_sdr=None):
     """Exact items everywhere; mask / filter gates over the bins the oracle itself is stable on. The bins on
-    which the device deviates must be oracle-unstable ones (two perturbations only sample the instability, so
-    up to 1 % of the bins may deviate without having been flagged), and the unstable set must stay small."""
+    which the device deviates must be oracle-unstable ones (three probes only sample the instability, so up to
+    1 % of the bins may deviate without having been flagged), and the unstable set is capped per case at what was
+    measured on B200 plus a margin. The WHOLE-waveform SDR gate is 40 dB, or -- on a segment where two builds of
+    the oracle itself agree to less than that (`order_sdr`) -- that level minus 3 dB."""
     assert got.error is None, (label, got.error)
     assert got.frames == want.frames
     assert got.ref_channel == want.ref_channel and got.zeroed_bins == want.zeroed_bins
@@ -264,21 +268,24 @@ def check_on_stable_bins(got, want, unstable, label, ll_gate, max_unstable=0.02,
     per_bin = dg.reshape(dg.shape[0], -1).max(axis=1)
     deviating = per_bin > 1e-2
     unexplained = deviating & ~unstable
-    assert unexplained.sum() <= (0.05 if max_unstable > 0.1 else 0.01) * len(unstable), (label, np.nonzero(unexplained)[0])
+    # three probes only sample the instability: 1 % of the bins may deviate unflagged (2 % where a third of the bins
+    # is chaotic for the oracle itself, the 40-iteration case)
+    assert unexplained.sum() <= (0.02 if max_unstable > 0.3 else 0.01) * len(unstable), (label, np.nonzero(unexplained)[0])
     s = ~(unstable | unexplained)
     e_gamma = rel_fro(got.posteriors[s], want.gamma[s])
     p999 = float(np.percentile(dg[s], 99.9))
     e_h = rel_fro(got.h[s], want.h[s])
     sdr = sdr_db(got.mono, want.mono)
     e_ll = abs(got.ll_final - want.ll_final) / abs(want.ll_final)
-    print(f"[{label}] unstable bins {np.nonzero(unstable)[0].tolist()} rel(gamma)={e_gamma:.2e} p99.9={p999:.2e} "
-          f"rel(h)={e_h:.2e} SDR={sdr:.1f} dB rel(ll)={e_ll:.2e}")
+    floor = 40.0 if order_sdr is None else min(40.0, order_sdr - 3.0)
+    print(f"[{label}] unstable bins {int(unstable.sum())}/{len(unstable)} (unexplained {int(unexplained.sum())}) "
+          f"rel(gamma)={e_gamma:.2e} p99.9={p999:.2e} rel(h)={e_h:.2e} SDR={sdr:.1f} dB "
+          f"(oracle vs its SIMD-Gram build: {'n/a' if order_sdr is None else '%.1f dB' % order_sdr}; gate {floor:.1f}) "
+          f"rel(ll)={e_ll:.2e}")
     assert e_gamma < 1e-3 and p999 < 1e-3 and e_h < 1e-3, (label, e_gamma, p999, e_h)
-    if cfg is None or not unstable.any():
-        assert sdr >= 40.0, (label, sdr)
-    else:
-        # a strong bin that is ill-conditioned for WPE dominates the waveform difference (the oracle agrees with
-        # ITSELF to 40 dB only on such a segment): the 40 dB gate is taken over the bins it is stable on
+    assert sdr >= floor, (label, sdr, order_sdr)
+    if cfg is not None and unstable.any():
+        # diagnostic: over the bins the oracle is stable on the waveforms agree far beyond 40 dB
         leak = unstable | unexplained  # the analysis window smears a bin over its two neighbours on each side
         for d in (1, 2):
             leak[d:] |= (unstable | unexplained)[:-d]
@@ -290,22 +297,36 @@ def check_on_stable_bins(got, want, unstable, label, ll_gate, max_unstable=0.02,
         assert e_ll < ll_gate, (label, e_ll)
 
 
-def test_enhance_cfg3_shape_ami_8ch_5class(gss, oracle):
+def check_segment(gss, oracle, simd_oracle, ss, cfg, label, max_abs, max_unstable, ll_gate_unstable=1e-3):
+    """One segment end to end: the strict gates when the oracle is stable on every bin, else the stable-bin gates."""
+    got = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
+    want = oracle_enhance(oracle, ss, cfg)
+    unstable = oracle_unstable_bins(oracle, ss, cfg)
+    order_sdr, order_flags = oracle_order_noise(oracle, simd_oracle, ss, cfg, want)
+    unstable |= order_flags
+    if unstable.any():
+        check_on_stable_bins(got, want, unstable, label, ll_gate_unstable, max_unstable, cfg, order_sdr)
+    else:
+        check_against_oracle(got, want, label, max_abs=max_abs)
+    return got
+
+
+def test_enhance_cfg3_shape_ami_8ch_5class(gss, oracle, simd_oracle):
     # BASELINE configs[2]: AMI-shaped, 8 channels, 4 speakers + noise, WPE taps 10 / delay 3, 20 iterations,
     # 40 s window. Two of the 257 bins (6.6 - 6.9 kHz, almost no speech energy) are chaotic over 20 EM
     # iterations: the oracle flips their masks under a 1e-7 perturbation of ITS OWN input.
     import synthbench as synth
     w = synth.workload("cfg3", n_segments=1)
-    ss, cfg = w.segments[0], w.cfg
-    got = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
+    got = check_segment(gss, oracle, simd_oracle, w.segments[0], w.cfg, "cfg3", max_abs=2e-2, max_unstable=0.02)
     assert got.frames == 5001
-    # ll_final sums every bin, the chaotic ones included (they settle in another local optimum): 1e-3 here
-    check_on_stable_bins(got, oracle_enhance(oracle, ss, cfg), oracle_unstable_bins(oracle, ss, cfg), "cfg3", 1e-3,
-                         cfg=cfg)
 
 
-@pytest.mark.parametrize("channels,speakers,iterations", [(2, 2, 5), (3, 4, 10), (5, 3, 40), (6, 2, 20), (8, 3, 5)])
-def test_enhance_sweep_shapes_channels_and_iterations(gss, oracle, channels, speakers, iterations):
+# (channels, speakers, iterations, cap on the fraction of oracle-unstable bins = measured on B200 + margin)
+SWEEP = [(2, 2, 5, 0.02), (3, 4, 10, 0.02), (5, 3, 40, SWEEP_5_3_40_CAP), (6, 2, 20, 0.10), (8, 3, 5, 0.02)]
+
+
+@pytest.mark.parametrize("channels,speakers,iterations,cap", SWEEP)
+def test_enhance_sweep_shapes_channels_and_iterations(gss, oracle, simd_oracle, channels, speakers, iterations, cap):
     # BASELINE configs[4] in miniature: channels 2-8, 2-4 speakers (+ noise), 5-40 EM iterations, WPE on, 4 s
     # of target speech in a 20 s window. Every (M, K) pair takes its own kernel specialisation (lanes per
     # frame, class tier). 40 iterations leave more bins chaotic in FP32 (for the oracle too) than 20 do.
@@ -314,12 +335,6 @@ def test_enhance_sweep_shapes_channels_and_iterations(gss, oracle, channels, spe
     cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(10, 2, 3, 0, 1e-10), True,
                                    iterations)
     ss = synth.make_supersegment(5000 + 10 * channels + speakers, channels, speakers, 4.0, 8.0, cfg)
-    got = gss.scheduler.enhance_batch(ss, cfg, diagnostics=True)
-    want = oracle_enhance(oracle, ss, cfg)
-    unstable = oracle_unstable_bins(oracle, ss, cfg)
-    label = f"sweep M={channels} S={speakers} I={iterations}"
-    if unstable.any():
-        print(f"[{label}] oracle self-SDR {oracle_self_sdr(oracle, ss, cfg, want):.1f} dB")
     # ll_final sums every bin, the unstable ones included: gated only when there are none
-    check_on_stable_bins(got, want, unstable, label, None if unstable.any() else 1e-4,
-                         max_unstable=0.5 if iterations > 20 else 0.10, cfg=cfg)
+    check_segment(gss, oracle, simd_oracle, ss, cfg, f"sweep M={channels} S={speakers} I={iterations}", max_abs=2e-2,
+                  max_unstable=cap, ll_gate_unstable=None)
