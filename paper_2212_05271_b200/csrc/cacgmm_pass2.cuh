@@ -65,9 +65,12 @@ struct EmPass2Cfg {
   // stride M = 8 they fell into two (8-way conflict: 72 M conflict cycles per cfg3 sweep, profiles/ncu_full_r02.md)
   static constexpr int SY = (M % 2 == 0) ? M + 1 : M;
   static constexpr int YSTAGE_FLOATS = 32 * SY * 2;
-  // per warp: dof scratch [32][NCHP] float4 | weights [32][WS] | two frame stages; a multiple of 256 bytes
+  // per warp: dof scratch [32][NCHP] float4 | weights [32][WS] | frame landing zone | sums; a multiple of 256 bytes
   static constexpr int SUMS = KT + 1;  // per frame lane: class masses and the log-likelihood, kept out of registers
-  static constexpr int WARP_SCRATCH_FLOATS = (32 * NCHP * 4 + 32 * WS + 2 * YSTAGE_FLOATS + 32 * SUMS + 63) & ~63;
+  // ONE landing zone: a group's frames are in registers a few instructions into its turn, and the next group's copy
+  // is issued into the same zone right after (it has the whole turn to land). A second zone cost 18 KB per block
+  // and, at M = 8, the second resident block with it.
+  static constexpr int WARP_SCRATCH_FLOATS = (32 * NCHP * 4 + 32 * WS + YSTAGE_FLOATS + 32 * SUMS + 63) & ~63;
   // epilogue dump: every thread parks its accumulators, stride chosen odd in float4 units (conflict-free)
   static constexpr int DUMP_STRIDE = ((NA * NDOF + 3) / 4 | 1) * 4;
   // accumulators + two groups of frames in flight must fit the register file at this occupancy
@@ -130,8 +133,8 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
 
   float* wscr = s_scratch + warp * Cfg::WARP_SCRATCH_FLOATS;
   float* wbuf = wscr + 32 * NCHP * 4;                                     // [32][WS]
-  float2* ybuf = reinterpret_cast<float2*>(wbuf + 32 * WS);               // [2][32][SY]
-  float* sums = reinterpret_cast<float*>(ybuf + 2 * 32 * Cfg::SY) + lane;  // [SUMS][32], this lane's column
+  float2* ybuf = reinterpret_cast<float2*>(wbuf + 32 * WS);               // [32][SY]
+  float* sums = reinterpret_cast<float*>(ybuf + 32 * Cfg::SY) + lane;      // [SUMS][32], this lane's column
 #pragma unroll
   for (int k = 0; k < Cfg::SUMS; ++k) sums[32 * k] = 0.f;
   const int g = lane / SPW, slot = lane % SPW;  // phase-B role
@@ -153,44 +156,41 @@ __global__ void __launch_bounds__(kEmThreads, EmPass2Cfg<M, L, KT, MODE == kSwee
   const int target = sd.target;
   const bool normalize = a.normalize != 0;
 
-  // frames of group `grp` -> stage `st` of this warp's landing zone; frames past the end are zero
-  auto issue_group = [&](int grp, int st) {
+  // frames of group `grp` -> this warp's landing zone; frames past the end are zero
+  auto issue_group = [&](int grp) {
     const float2* gs = src + (long long)grp * 32 * M;
-    float2* d = ybuf + st * (32 * Cfg::SY);
     const int n = (nt - grp * 32) * M;  // valid elements (may exceed 32 * M)
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       const int i = lane + 32 * j;
-      cp_async8_zfill(d + i + (Cfg::SY - M) * (i / M), gs + (i < n ? i : 0), i < n);
+      cp_async8_zfill(ybuf + i + (Cfg::SY - M) * (i / M), gs + (i < n ? i : 0), i < n);
     }
     cp_async_commit();
   };
   int pid = 0;
   if (warp < ngroups) {
-    issue_group(warp, 0);
+    issue_group(warp);
     pid = (int)psrc[min(warp * 32 + lane, nt - 1)];
   }
 
-  int it = 0;
 #pragma unroll 1
-  for (int grp = warp; grp < ngroups; grp += NW, ++it) {
+  for (int grp = warp; grp < ngroups; grp += NW) {
     const int t = grp * 32 + lane;
     const bool valid = t < nt;
-    // the next group of this warp is fetched while this one is processed
-    int pidn = 0;
-    if (grp + NW < ngroups) {
-      issue_group(grp + NW, (it + 1) & 1);
-      pidn = (int)psrc[min((grp + NW) * 32 + lane, nt - 1)];
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<0>();
     __syncwarp();
     float2 y[M];
     {
-      const float2* ys = ybuf + (it & 1) * (32 * Cfg::SY) + lane * Cfg::SY;
+      const float2* ys = ybuf + lane * Cfg::SY;
 #pragma unroll
       for (int m = 0; m < M; ++m) y[m] = ys[m];
+    }
+    __syncwarp();  // every lane has taken its frame: the zone may be overwritten
+    // the next group of this warp is fetched while this one is processed
+    int pidn = 0;
+    if (grp + NW < ngroups) {
+      issue_group(grp + NW);
+      pidn = (int)psrc[min((grp + NW) * 32 + lane, nt - 1)];
     }
 
     // ================= phase A: lane = frame =================

@@ -59,7 +59,7 @@ def check_against_oracle(got, want, label="", max_abs=2e-2):
 
 CFG2_MAX_ABS = 4e-3       # measured 1.8e-3 on B200 (segment 0)
 CFG4_MAX_ABS = 2e-2       # only used if the oracle is stable on every bin of the segment
-SWEEP_5_3_40_CAP = 0.50   # 40 iterations: measured below
+SWEEP_5_3_40_CAP = 0.45   # 40 iterations: 104 of 257 bins measured on B200
 
 
 def test_enhance_tiny_batch_with_wpe(gss, oracle):
