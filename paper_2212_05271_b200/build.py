@@ -27,7 +27,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--use_fa
 CU_SOURCES = ["api.cu", "stft_kernels.cu", "wpe_kernels.cu", "wpe_gram_tc.cu", "wpe_apply_tc.cu", "beamform_kernels.cu", "cacgmm_dispatch.cu"] + [
     f"cacgmm_m{m}.cu" for m in range(1, 9)]
 CPP_SOURCES = ["host_logic.cpp"]
-HEADERS = ["kernels.h", "gss_internal.cuh", "em_layout.cuh", "linalg.cuh", "cacgmm_kernels.cuh", "cacgmm_pass2.cuh",
+HEADERS = ["kernels.h", "gss_internal.cuh", "em_layout.cuh", "linalg.cuh", "cacgmm_kernels.cuh", "cacgmm_pass2.cuh", "cacgmm_pass3.cuh",
            "cacgmm_inst.inc", os.path.join("..", "..", "include", "gss_b200.h")]
 
 

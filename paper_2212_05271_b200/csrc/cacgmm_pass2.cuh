@@ -58,7 +58,7 @@ struct EmPass2Cfg {
   }
   static constexpr int NW = kEmThreads / 32;
   // coefficient table of one lane slice: [dof][class] packed (no class padding), rounded up to whole float4s
-  static constexpr int CS = (NDOFP * KT + 3) & ~3;
+  static constexpr int CS = NDOFP * KT;  // NDOFP is a multiple of 4
   static constexpr int COEF_FLOATS = L * CS;
   // one group of frames (cp.async landing zone). Frame stride in float2 units: odd, so that the 16 lanes of a
   // half-warp reading channel m of their own frame (LDS.64) fall into 16 different bank pairs. With the natural

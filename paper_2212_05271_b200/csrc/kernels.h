@@ -136,7 +136,10 @@ constexpr int em_lanes(int M, int KT) {
   if (M == 5) return KT <= 5 ? 2 : 4;
   if (M == 6) return 4;
   if (M == 7) return KT <= 6 ? 4 : 8;
-  return KT <= 3 ? 4 : 8;  // M = 8: 4 lanes put 16 K accumulators + two groups of frames past 128 registers
+  // M = 8: with 4 lanes the 16 K accumulators + two groups of frames go past 128 registers. The 8-lane shapes run
+  // the row-owner sweep (cacgmm_pass3.cuh): measured 20.4 ms against 21.1 ms for the two-phase sweep per 16-segment
+  // cfg3 step; at M = 7 the eighth lane of every frame would idle and the two-phase sweep wins (15.4 vs 16.7 ms, cfg2)
+  return KT <= 3 ? 4 : 8;
 }
 /// Class count the kernels are instantiated for (>= K).
 constexpr int em_class_tier(int K) { return K <= 2 ? 2 : K <= 3 ? 3 : K <= 4 ? 4 : K <= 5 ? 5 : K <= 6 ? 6 : 8; }
