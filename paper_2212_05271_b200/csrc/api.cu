@@ -76,11 +76,22 @@ struct gss_b200_ctx {
   int wpe_apply_tc = 1;      // GSS_B200_WPE_APPLY=fp32 selects the FP32-FMA prediction kernel instead of tcgen05
   int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
   int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
+  // Shape groups of one batch (segments sharing channel count and class tier) are independent: they are enqueued
+  // on up to kGroupStreams streams so that one group's latency-bound kernels (FP64 update / solve, small grids)
+  // run beside another group's sweeps. GSS_B200_GROUP_STREAMS=1 puts everything back on `stream`.
+  static constexpr int kGroupStreams = 4;
+  cudaStream_t side[kGroupStreams - 1] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr, join_ev[kGroupStreams - 1] = {nullptr, nullptr, nullptr};
+  int group_streams = kGroupStreams;
+  cudaStream_t active = nullptr;  // stream the stage drivers launch on (null: `stream`)
   bool dev_call = false;     // inside a *_dev entry point: tensors are device memory, completion is an event
   long long nvtx_ranges = 0; // NVTX ranges opened by this context (gss_b200_nvtx_range_count)
 };
 
 namespace {
+
+/// Stream the stage drivers (and the per-kernel clocks) enqueue on.
+inline cudaStream_t S(gss_b200_ctx* c) { return c->active ? c->active : c->stream; }
 
 gss_status fail(gss_b200_ctx* c, gss_status code, const std::string& msg, long long freq = -1) {
   if (c) {
@@ -103,11 +114,11 @@ struct KClock {
     cudaEvent_t a;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    cudaEventRecord(a, c->stream);
+    cudaEventRecord(a, S(c));
     c->prof_recs.push_back({id, a, b});
   }
   ~KClock() {
-    if (b) cudaEventRecord(b, c->stream);
+    if (b) cudaEventRecord(b, S(c));
   }
 };
 /// NVTX range on the calling host thread, named after the reference's stage keys ("gss.stft", "gss.wpe", ...):
@@ -532,7 +543,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first
       any = true;
     } else {  // pass-through (wpe.hpp:108-112)
       CU_TRY(c, cudaMemcpyAsync(g.Yd + d.y_off, g.Y + d.y_off, sizeof(float2) * (size_t)g.F * d.T * g.M,
-                                cudaMemcpyDeviceToDevice, c->stream));
+                                cudaMemcpyDeviceToDevice, S(c)));
     }
   }
   if (!any) return GSS_OK;
@@ -564,11 +575,11 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first
   for (int it = 0; it < w.iterations; ++it) {
     a.ycur = it == 0 ? g.Y : g.Yd;
     a.w_next = fuse_power && it + 1 < w.iterations ? g.w : nullptr;
-    CU_TRY(c, cudaMemsetAsync(g.fb_ticket, 0, sizeof(int) * kWpeFallbackSlots, c->stream));
+    CU_TRY(c, cudaMemsetAsync(g.fb_ticket, 0, sizeof(int) * kWpeFallbackSlots, S(c)));
     for (int step = 0; step < 4; ++step) {
       if (step == 0 && w_ready) continue;
       KClock k(c, kK_wpe_power + step);
-      CU_TRY(c, launch_wpe_step(step, a, count, g.F, g.max_T, g.max_wchunks, c->stream));
+      CU_TRY(c, launch_wpe_step(step, a, count, g.F, g.max_T, g.max_wchunks, S(c)));
     }
     w_ready = a.w_next != nullptr;
   }
@@ -604,7 +615,7 @@ gss_status run_em(gss_b200_ctx* c, Group& g, const EmRun& r) {
   u.mode = r.from_state ? kEmFromState : kEmInit;
   {
     KClock k(c, kK_em_update);
-    CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+    CU_TRY(c, launch_em_update(shape, u, g.nseg, S(c)));
   }
   EmPassArgs p;
   p.y = r.tensor;
@@ -622,30 +633,30 @@ gss_status run_em(gss_b200_ctx* c, Group& g, const EmRun& r) {
   for (int it = 0; it < I; ++it) {
     {
       KClock k(c, kK_em_pass);
-      CU_TRY(c, launch_em_pass(shape, false, p, g.nwork, g.F, c->stream));
+      CU_TRY(c, launch_em_pass(shape, false, p, g.nwork, g.F, S(c)));
     }
     u.mode = kEmMstep;
     u.bin_ll = g.bin_ll + (long long)it * g.nF;
     {
       KClock k(c, kK_em_update);
-      CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+      CU_TRY(c, launch_em_update(shape, u, g.nseg, S(c)));
     }
   }
   p.gamma = g.gamma;
   {
     KClock k(c, kK_em_pass);
-    CU_TRY(c, launch_em_pass(shape, r.final_stats, p, g.nwork, g.F, c->stream));
+    CU_TRY(c, launch_em_pass(shape, r.final_stats, p, g.nwork, g.F, S(c)));
   }
   u.mode = kEmFinal;
   u.bin_ll = g.bin_ll + (long long)I * g.nF;
   {
     KClock k(c, kK_em_update);
-    CU_TRY(c, launch_em_update(shape, u, g.nseg, c->stream));
+    CU_TRY(c, launch_em_update(shape, u, g.nseg, S(c)));
   }
   for (int it = r.all_ll ? 0 : I; it <= I; ++it) {
     KClock k(c, kK_misc);
     CU_TRY(c, launch_sum_ll(g.bin_ll + (long long)it * g.nF, g.seg_ll + (long long)it * g.nseg, g.d_segs, g.nseg,
-                            g.F, c->stream));
+                            g.F, S(c)));
   }
   return GSS_OK;
 }
@@ -666,11 +677,11 @@ gss_status run_mvdr_design(gss_b200_ctx* c, Group& g, int fixed_ref, bool have_t
   a.fixed_ref = fixed_ref;
   {
     KClock k(c, kK_mvdr);
-    CU_TRY(c, launch_select_reference(a, g.nseg, c->stream));
+    CU_TRY(c, launch_select_reference(a, g.nseg, S(c)));
   }
   {
     KClock k(c, kK_mvdr);
-    CU_TRY(c, launch_mvdr_solve(a, g.nseg, c->stream));
+    CU_TRY(c, launch_mvdr_solve(a, g.nseg, S(c)));
   }
   return GSS_OK;
 }
@@ -780,6 +791,13 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
     delete c;
     return fail(nullptr, GSS_CUDA_ERROR, cudaGetErrorString(e));
   }
+  if (const char* sg = std::getenv("GSS_B200_GROUP_STREAMS"))
+    c->group_streams = std::min<int>(gss_b200_ctx::kGroupStreams, std::max(1, std::atoi(sg)));
+  bool side_ok = cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) == cudaSuccess;
+  for (int i = 0; i < gss_b200_ctx::kGroupStreams - 1 && side_ok; ++i)
+    side_ok = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&c->join_ev[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!side_ok) c->group_streams = 1;  // the single-stream path needs none of them
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     unsigned long long thr = ~0ull;  // keep freed blocks cached for the next batch
@@ -803,6 +821,14 @@ void gss_b200_destroy(gss_b200_ctx* c) {
   cudaStreamSynchronize(c->stream);
   cudaStreamSynchronize(c->copy_stream);
   cudaStreamDestroy(c->copy_stream);
+  for (int i = 0; i < gss_b200_ctx::kGroupStreams - 1; ++i) {
+    if (c->side[i]) {
+      cudaStreamSynchronize(c->side[i]);
+      cudaStreamDestroy(c->side[i]);
+    }
+    if (c->join_ev[i]) cudaEventDestroy(c->join_ev[i]);
+  }
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   for (auto& kv : c->tables) {
     cudaFree(kv.second.tw);
     cudaFree(kv.second.win);
@@ -1050,10 +1076,28 @@ gss_status run_impl(gss_b200_ctx* c, gss_b200_batch* b) {
   const gss_pipeline_config& cfg = b->cfg;
   const StftParams sp = stft_params(cfg.stft);
   int gi = 0;
+  // fork: several shape groups -> several streams (see gss_b200_ctx::side); joined again below and on every exit
+  const int nstreams = std::min<int>((int)b->groups.size(), c->group_streams);
+  struct Join {
+    gss_b200_ctx* c;
+    int n;
+    ~Join() {
+      c->active = nullptr;
+      for (int i = 1; i < n; ++i) {
+        cudaEventRecord(c->join_ev[i - 1], c->side[i - 1]);
+        cudaStreamWaitEvent(c->stream, c->join_ev[i - 1], 0);
+      }
+    }
+  } join{c, nstreams};
+  if (nstreams > 1) {
+    cudaEventRecord(c->fork_ev, c->stream);
+    for (int i = 1; i < nstreams; ++i) cudaStreamWaitEvent(c->side[i - 1], c->fork_ev, 0);
+  }
   for (auto& gp : b->groups) {
     Group& g = *gp;
+    c->active = nstreams > 1 && gi % nstreams > 0 ? c->side[gi % nstreams - 1] : nullptr;
     cudaEvent_t* ev = &b->events[2 + 6 * gi++];
-    cudaStream_t st = c->stream;
+    cudaStream_t st = S(c);
     // device-side state that a previous run of the same batch may have touched
     CU_TRY(c, cudaMemsetAsync(g.status, 0xFF, sizeof(status_t) * g.nseg, st));
     CU_TRY(c, cudaMemsetAsync(g.zeroed, 0, sizeof(int) * g.nseg, st));
