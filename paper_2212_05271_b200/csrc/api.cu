@@ -1077,7 +1077,8 @@ gss_status run_impl(gss_b200_ctx* c, gss_b200_batch* b) {
   const StftParams sp = stft_params(cfg.stft);
   int gi = 0;
   // fork: several shape groups -> several streams (see gss_b200_ctx::side); joined again below and on every exit
-  const int nstreams = std::min<int>((int)b->groups.size(), c->group_streams);
+  // (per-kernel event clocks are only meaningful for serialised launches: profiling keeps everything on one stream)
+  const int nstreams = c->prof_on ? 1 : std::min<int>((int)b->groups.size(), c->group_streams);
   struct Join {
     gss_b200_ctx* c;
     int n;

@@ -97,3 +97,48 @@ def test_two_rank_gloo_gather_is_ordered():
     owners = {o[1]: o[2] for o in out0}
     assert sorted(calls0[0] + calls1[0]) == list(range(23))  # every segment enhanced exactly once
     assert all(owners[i] == 0 for i in calls0[0]) and all(owners[i] == 1 for i in calls1[0])
+
+
+def test_sweep_sample_partition_covers_every_segment_once_and_balances():
+    """The strong-scaling entry of bench.py's `configs` block: a sample of the 4096-segment sweep (BASELINE configs[4])
+    split over N ranks with sharding.shard on the SURVEY 8e cost model. Every rank draws the same parameter list, so
+    the shards are disjoint, cover the sample, and their modelled loads stay within a few percent of each other."""
+    import synthbench as synth
+    params = synth.sweep_params(4096)
+    assert len(params) == 4096 and params == synth.sweep_params(4096)          # same list on every rank
+    assert {p[1] for p in params} == set(range(2, 9)) and {p[4] for p in params} == {5, 10, 20, 40}
+    assert all(2 <= p[2] <= 4 and 2.0 <= p[3] <= 12.0 for p in params)
+    sample = params[::16][:256]
+    costs = [sharding.segment_cost(synth.sweep_frames(p[3]), p[1], p[2] + 1, p[4], 10, 3) for p in sample]
+    for world in (1, 2, 4, 8):
+        owned = sharding.shard(costs, world)
+        assert sorted(i for o in owned for i in o) == list(range(256))
+        loads = [sum(costs[i] for i in o) for o in owned]
+        assert sum(loads) / (world * max(loads)) > 0.97, (world, loads)
+
+
+def test_bench_relaunches_itself_as_n_ranks(monkeypatch):
+    """`python bench.py --gpus N` without a torchrun environment must become N ranks (one per GPU); under torchrun
+    (WORLD_SIZE set) it must not fork again."""
+    import importlib.util
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("gss_bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    seen = {}
+
+    def fake_call(cmd):
+        seen["cmd"] = cmd
+        return 0
+
+    monkeypatch.setattr(bench.subprocess, "call", fake_call)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2", "--headline-only"])
+    with pytest.raises(SystemExit) as e:
+        bench.main()
+    assert e.value.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node" in cmd
+    assert cmd[cmd.index("--nproc-per-node") + 1] == "4" and cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-5:] == ["--gpus", "4", "--steps", "2", "--headline-only"] and cmd[-6].endswith("bench.py")

@@ -87,7 +87,7 @@ def read_raw(rep):
     return rows[0], rows[1], rows[2:]
 
 
-def full(reps, segments, out, traffic_path):
+def full(reps, segments, out, traffic_path, label="cfg2"):
     lines = []
     traffic = {}
     for rep in reps:
@@ -116,9 +116,10 @@ def full(reps, segments, out, traffic_path):
             t["us"].append(rec["time"])
     with open(out, "w") as f:
         f.write("# ncu `--set full --clock-control none` captures (one row per captured launch)\n\n")
-        f.write("Profiled command: `python bench.py --steps 1 --warmup 3 --no-cpu-baseline` (cfg2, %d segments). "
-                "Durations are under the profiler (replayed, cold cache) and are NOT bench values.\n\n" % segments)
-        f.write("| kernel | time us | DRAM rd MB | DRAM wr MB | DRAM %% | SM %% | issue %% | fma pipe %% | fp64 %% | tensor %% | occupancy %% | regs | grid x block | report |\n")
+        f.write("Profiled command: `python bench.py --steps 1 --warmup 3 --no-cpu-baseline --headline-only --workload %s "
+                "--segments %d`. Durations are under the profiler (replayed, cold cache) and are NOT bench values.\n\n"
+                % (label, segments))
+        f.write("| kernel | time us | DRAM rd MB | DRAM wr MB | DRAM % | SM % | issue % | fma pipe % | fp64 % | tensor % | occupancy % | regs | grid x block | report |\n")
         f.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
 
         def fm(v, s="%.1f"):
@@ -146,8 +147,9 @@ if __name__ == "__main__":
     ap.add_argument("--segments", type=int, default=16)
     ap.add_argument("--out", default=None)
     ap.add_argument("--traffic", default=None)
+    ap.add_argument("--label", default="cfg2", help="workload name of the profiled command")
     a = ap.parse_args()
     if a.mode == "launches":
         launches(a.paths[0], a.paths[1])
     else:
-        full(a.paths, a.segments, a.out, a.traffic)
+        full(a.paths, a.segments, a.out, a.traffic, a.label)
