@@ -29,6 +29,9 @@
 
 namespace gssb {
 
+// 8 warps: at 10 or 12 the 168 registers left per thread spill (26.2 / 22.7 vs 20.4 ms per 16-segment cfg3 step)
+constexpr int kEm3Threads = 256;
+
 template <int M, int KT, bool FINAL>
 struct EmPass3Cfg {
   static constexpr int L = 8;
@@ -39,7 +42,7 @@ struct EmPass3Cfg {
   static constexpr int NA = FINAL ? 2 : KT;
   static constexpr int WS = FINAL ? 2 : KT;                  // weights per frame
   static constexpr int SPW = 4, NSTEP = 8;                   // frames per step, steps per group
-  static constexpr int NW = kEmThreads / 32;
+  static constexpr int NW = kEm3Threads / 32;
   static constexpr int NQ = KT + 1;                          // exchanged per (frame, row): K partial forms + |y_g|^2
   static constexpr int NPL = (NQ + 3) / 4;                   // float4 planes of the exchange buffer
   static constexpr int WPL = (WS + 3) / 4;                   // float4 planes of the weight buffer
@@ -51,7 +54,7 @@ struct EmPass3Cfg {
 };
 
 template <int M, int KT, int MODE>
-__global__ void __launch_bounds__(kEmThreads, 1) em_pass3_kernel(EmPassArgs a) {
+__global__ void __launch_bounds__(kEm3Threads, 1) em_pass3_kernel(EmPassArgs a) {
   constexpr bool FINAL = MODE == kSweepFinal;
   using Cfg = EmPass3Cfg<M, KT, FINAL>;
   using Lay = EmLayout<M, 8>;
@@ -79,11 +82,11 @@ __global__ void __launch_bounds__(kEmThreads, 1) em_pass3_kernel(EmPassArgs a) {
   // ---- tables of this (segment, bin)
   {
     const float* cks = a.ck + sd.tab_off + (long long)f * sd.npat * KT;
-    for (int i = tid; i < sd.npat * KTP; i += kEmThreads) {
+    for (int i = tid; i < sd.npat * KTP; i += kEm3Threads) {
       const int k = i % KTP, p = i / KTP;
       s_ck[i] = k < KT ? cks[p * KT + k] : -CUDART_INF_F;
     }
-    for (int p = tid; p < sd.npat; p += kEmThreads) {
+    for (int p = tid; p < sd.npat; p += kEm3Threads) {
       unsigned m = 0;
       for (int k = 0; k < KT; ++k)
         if (cks[p * KT + k] != -CUDART_INF_F) m |= 1u << k;
@@ -317,32 +320,36 @@ __global__ void __launch_bounds__(kEmThreads, 1) em_pass3_kernel(EmPassArgs a) {
     __syncwarp();
 
     // ================= phase 3: lane = (slot, row) =================
-    {
-      float w[NSTEP][4 * WPL];
+    // in PH passes of NSTEP / PH steps each: the pass's weights in registers, then class-outer accumulation
+    constexpr int PH = 1;  // (two passes of four steps: 20.2 vs 20.4 ms, within noise)
+    constexpr int HS = NSTEP / PH;
 #pragma unroll
-      for (int s = 0; s < NSTEP; ++s)
+    for (int h = 0; h < PH; ++h) {
+      float w[HS][4 * WPL];
+#pragma unroll
+      for (int s = 0; s < HS; ++s)
 #pragma unroll
         for (int p = 0; p < WPL; ++p)
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(w[s][4 * p]), "=f"(w[s][4 * p + 1]), "=f"(w[s][4 * p + 2]), "=f"(w[s][4 * p + 3])
-                       : "r"(wofs + (unsigned)(p * 512 + (s * SPW + slot) * 16))
+                       : "r"(wofs + (unsigned)(p * 512 + ((h * HS + s) * SPW + slot) * 16))
                        : "memory");
       if (FINAL) {
 #pragma unroll
-        for (int s = 0; s < NSTEP; ++s)
+        for (int s = 0; s < HS; ++s)
 #pragma unroll
           for (int j = 0; j < NDOF; ++j) {
-            acc[0][j] = fmaf(w[s][0], P[s][j], acc[0][j]);
-            acc[NA - 1][j] = fmaf(w[s][1], P[s][j], acc[NA - 1][j]);
+            acc[0][j] = fmaf(w[s][0], P[h * HS + s][j], acc[0][j]);
+            acc[NA - 1][j] = fmaf(w[s][1], P[h * HS + s][j], acc[NA - 1][j]);
           }
       } else {
 #pragma unroll
         for (int k = 0; k < NA; ++k) {
           if (am & (1u << k)) {  // warp-uniform: classes inactive for all 32 frames are skipped
 #pragma unroll
-            for (int s = 0; s < NSTEP; ++s)
+            for (int s = 0; s < HS; ++s)
 #pragma unroll
-              for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w[s][k], P[s][j], acc[k][j]);
+              for (int j = 0; j < NDOF; ++j) acc[k][j] = fmaf(w[s][k], P[h * HS + s][j], acc[k][j]);
           }
         }
       }
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(kEmThreads, 1) em_pass3_kernel(EmPassArgs a) {
   __syncthreads();
   const long long cell = sd.cell_off + (long long)f * sd.nchunks + wi.chunk;
   float* out = a.part + cell * a.cell_stride;
-  for (int i = tid; i < PL::CELL; i += kEmThreads) {
+  for (int i = tid; i < PL::CELL; i += kEm3Threads) {
     const int gg = i / PL::STRIDE, e = i - gg * PL::STRIDE;
     float s = 0.f;
     if (e < PL::ACC) {
