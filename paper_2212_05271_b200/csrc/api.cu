@@ -53,8 +53,9 @@ struct gss_b200_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // audio uploads, wave by wave, under the previous wave's kernels
-  int waves = 2;                       // GSS_B200_WAVES
-  double wave_first_frac = 0.25;       // GSS_B200_WAVE_FIRST_PCT: share of the audio in the first wave
+  int waves = 3;                       // GSS_B200_WAVES
+  double wave_first_frac = 0.0;        // GSS_B200_WAVE_FIRST_PCT: share of the audio in the first wave (0: from the growth)
+  double wave_growth = 4.0;            // GSS_B200_WAVE_GROWTH: each wave this many times the previous one
   long long wave_min_floats = 2 << 20; // GSS_B200_WAVE_MIN_FLOATS: no wave smaller than this (8 MB)
   std::string err;
   long long err_freq = -1;
@@ -811,6 +812,7 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
   if (const char* s = std::getenv("GSS_B200_WAVE_MIN_FLOATS")) c->wave_min_floats = std::max(1LL, std::atoll(s));
   if (const char* s = std::getenv("GSS_B200_WAVE_FIRST_PCT"))
     c->wave_first_frac = std::min(100, std::max(1, std::atoi(s))) * 0.01;
+  if (const char* s = std::getenv("GSS_B200_WAVE_GROWTH")) c->wave_growth = std::min(64.0, std::max(1.0, std::atof(s)));
   *out = c;
   return GSS_OK;
 }
@@ -1018,23 +1020,28 @@ gss_status upload_impl(gss_b200_ctx* c, int32_t n, const gss_segment_desc* segs,
       free_batch(c, b);
       return rc;
     }
-    // Waves of whole segments. Only the first wave's upload is exposed, so it is small: a quarter of the audio,
-    // whose STFT + WPE (about 4x the bus time per byte on the headline shape) cover the upload of the rest.
-    // Small launches pay in tail effects, so there are two waves by default, and none below ~8 MB.
+    // Waves of whole segments. Only the first wave's upload is exposed, so it is small; the STFT + WPE of a wave
+    // take about 4x the bus time of its bytes on the headline shapes, so every wave may be ~4x the previous one and
+    // still have its upload covered: three waves of 1 : 4 : 16 (5 % of the audio exposed). Small launches pay in
+    // tail effects, so no wave is below ~8 MB.
     {
       long long floats = 0;
       for (int j = 0; j < g->nseg; ++j) floats += (long long)g->M * g->segs[j].N;
       const long long min_wave = c->wave_min_floats;
-      const long long first = std::max<long long>((long long)(floats * c->wave_first_frac), min_wave);
-      const long long rest = c->waves > 1 ? std::max<long long>((floats - first) / (c->waves - 1), min_wave) : 0;
-      long long acc = 0, target = c->waves > 1 ? first : floats + 1;
+      double geo = 0.0, term = 1.0;
+      for (int w = 0; w < c->waves; ++w, term *= c->wave_growth) geo += term;
+      const double first_frac = c->wave_first_frac > 0.0 ? c->wave_first_frac : 1.0 / geo;
+      long long acc = 0;
+      double want = std::max<double>((double)floats * first_frac, (double)min_wave);
+      long long target = c->waves > 1 ? (long long)want : floats + 1;
       g->wave_first.push_back(0);
       for (int j = 0; j < g->nseg; ++j) {
         acc += (long long)g->M * g->segs[j].N;
         if (acc >= target && j + 1 < g->nseg && (int)g->wave_first.size() < c->waves) {
           g->wave_first.push_back(j + 1);
           acc = 0;
-          target = rest;
+          want = std::max<double>(want * c->wave_growth, (double)min_wave);
+          target = (long long)want;
         }
       }
       g->wave_first.push_back(g->nseg);
