@@ -44,9 +44,8 @@ struct EmPass3Cfg {
   static constexpr int SPW = 4, NSTEP = 8;                   // frames per step, steps per group
   static constexpr int NW = kEm3Threads / 32;
   static constexpr int NQ = KT + 1;                          // exchanged per (frame, row): K partial forms + |y_g|^2
-  static constexpr int NPL = (NQ + 3) / 4;                   // float4 planes of the exchange buffer
   static constexpr int WPL = (WS + 3) / 4;                   // float4 planes of the weight buffer
-  static constexpr int EXCH_BYTES = NPL * 32 * 8 * 16;       // [plane][frame][slot] float4
+  static constexpr int EXCH_BYTES = NQ * 32 * 8 * 4;         // [quantity][frame][row] float: one 1 KB plane per class
   static constexpr int W_BYTES = WPL * 32 * 16;              // [plane][frame] float4
   static constexpr int Y_BYTES = 32 * M * 8;                 // [frame][channel] float2, natural stride
   static constexpr int WARP_SCRATCH_BYTES = (EXCH_BYTES + W_BYTES + Y_BYTES + 127) & ~127;
@@ -59,7 +58,7 @@ __global__ void __launch_bounds__(kEm3Threads, 1) em_pass3_kernel(EmPassArgs a) 
   using Cfg = EmPass3Cfg<M, KT, FINAL>;
   using Lay = EmLayout<M, 8>;
   constexpr int L = 8, NDOF = Cfg::NDOF, KTP = Cfg::KTP, NA = Cfg::NA, NW = Cfg::NW;
-  constexpr int NSTEP = Cfg::NSTEP, SPW = Cfg::SPW, NPL = Cfg::NPL, WPL = Cfg::WPL;
+  constexpr int NSTEP = Cfg::NSTEP, SPW = Cfg::SPW, WPL = Cfg::WPL;
   constexpr int D = Lay::D, HALF = Lay::HALF;
   using PL = PartLayout<M, L, KT, NA>;
   extern __shared__ float4 smem_f4[];
@@ -112,11 +111,12 @@ __global__ void __launch_bounds__(kEm3Threads, 1) em_pass3_kernel(EmPassArgs a) 
   const unsigned wofs = wbase + Cfg::EXCH_BYTES;                 // weights [plane][frame] float4
   const unsigned yofs = wofs + Cfg::W_BYTES;                     // frames  [frame][channel] float2
   float2* ybuf = reinterpret_cast<float2*>(s_scr + (size_t)warp * Cfg::WARP_SCRATCH_BYTES + Cfg::EXCH_BYTES + Cfg::W_BYTES);
-  // exchange addressing. Slot of row g in frame fr: g ^ (fr & 7). Phase 1 (fr = 4 s + slot): the low three bits of
-  // fr are ((s & 1) << 2) | slot, so a lane needs two addresses, for even and odd steps; phase 2 (fr = lane): one
-  // address XOR (g << 4) with g a compile-time constant.
-  const unsigned ex_st = wbase + (unsigned)slot * 128u + (unsigned)((g ^ slot) << 4);
-  const unsigned ex_ld = wbase + (unsigned)lane * 128u + (unsigned)((lane & 7) << 4);
+  // exchange addressing: plane q (class, or the norm) holds [frame][row] floats, 32 bytes per frame. A phase-1 store
+  // (one class, one step) is 32 lanes x 4 bytes = 128 contiguous bytes; phase 2 (lane = frame) reads its frame's two
+  // 16-byte halves, and the halves of frames 4..7 (mod 8) are swapped so that a quarter-warp covers all 32 banks:
+  // row g of frame fr sits at float (g ^ 4 ((fr >> 2) & 1)); in phase 1 fr >> 2 is the step number.
+  const unsigned ex_st0 = wbase + (unsigned)(slot * 32 + g * 4), ex_st1 = wbase + (unsigned)(slot * 32 + (g ^ 4) * 4);
+  const unsigned ex_ld = wbase + (unsigned)(lane * 32 + ((lane >> 2) & 1) * 16);
   // channel addresses of this row and of its partners (frame `slot` of a step)
   const unsigned y_x = yofs + (unsigned)(slot * M + row) * 8u;
   unsigned y_z[D + HALF > 0 ? D + HALF : 1];
@@ -163,8 +163,12 @@ __global__ void __launch_bounds__(kEm3Threads, 1) em_pass3_kernel(EmPassArgs a) 
     cp_async_wait<0>();
     __syncwarp();
 
+    // classes that are active in at least one of the group's 32 frames: the others have gamma == 0 throughout, so
+    // neither their quadratic forms (phase 1) nor their accumulation (phase 3) is evaluated
+    const unsigned am = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid]);
+
     // ================= phase 1: lane = (slot, row) =================
-    // the channels of step s + 1 are requested before the arithmetic of step s (register double buffer)
+    // 1a: the row's dofs of the 8 steps (the channels of step s + 1 are requested before the arithmetic of step s)
     float P[NSTEP][NDOF];
     constexpr int NZ = D + HALF > 0 ? D + HALF : 1;
     float2 xb[2], zb[2][NZ];
@@ -191,23 +195,28 @@ __global__ void __launch_bounds__(kEm3Threads, 1) em_pass3_kernel(EmPassArgs a) 
         const float a1 = lo_half ? x.x : x.y, a2 = lo_half ? x.y : -x.x;
         P[s][M - 1] = fmaf(a1, z[D].x, a2 * z[D].y);
       }
-      float pq[4 * NPL];
+      // this row's share of |y|^2 (plane KT)
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(((s & 1) ? ex_st1 : ex_st0) + (unsigned)(KT * 1024 + s * 128)),
+                   "f"(owner ? P[s][0] : 0.f)
+                   : "memory");
+    }
+    // 1b: class-outer partial forms: 8 independent chains (one per step) per active class
 #pragma unroll
-      for (int k = 0; k < 4 * NPL; ++k) pq[k] = 0.f;
+    for (int k = 0; k < KT; ++k) {
+      if (am & (1u << k)) {  // warp-uniform
+        float v[NSTEP];
 #pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        float v = cf[k][0] * P[s][0];
+        for (int s = 0; s < NSTEP; ++s) v[s] = cf[k][0] * P[s][0];
 #pragma unroll
-        for (int j = 1; j < NDOF; ++j) v = fmaf(cf[k][j], P[s][j], v);
-        pq[k] = v;
+        for (int j = 1; j < NDOF; ++j)
+#pragma unroll
+          for (int s = 0; s < NSTEP; ++s) v[s] = fmaf(cf[k][j], P[s][j], v[s]);
+#pragma unroll
+        for (int s = 0; s < NSTEP; ++s)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(((s & 1) ? ex_st1 : ex_st0) + (unsigned)(k * 1024 + s * 128)),
+                       "f"(v[s])
+                       : "memory");
       }
-      pq[KT] = owner ? P[s][0] : 0.f;  // this row's share of |y|^2
-      const unsigned ea = (ex_st ^ (unsigned)((s & 1) << 6)) + (unsigned)(s * SPW * 128);
-#pragma unroll
-      for (int p = 0; p < NPL; ++p)
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ea + (unsigned)(p * 4096)), "f"(pq[4 * p]),
-                     "f"(pq[4 * p + 1]), "f"(pq[4 * p + 2]), "f"(pq[4 * p + 3])
-                     : "memory");
     }
     __syncwarp();  // partial forms visible; every lane has taken its channels: the landing zone may be overwritten
     int pidn = 0;
@@ -217,31 +226,22 @@ __global__ void __launch_bounds__(kEm3Threads, 1) em_pass3_kernel(EmPassArgs a) 
     }
 
     // ================= phase 2: lane = frame =================
+    auto row_sum = [&](int plane) {  // the 8 rows' shares of one quantity for this lane's frame
+      float4 u0, u1;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(u0.x), "=f"(u0.y), "=f"(u0.z), "=f"(u0.w)
+                   : "r"(ex_ld + (unsigned)(plane * 1024))
+                   : "memory");
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(u1.x), "=f"(u1.y), "=f"(u1.z), "=f"(u1.w)
+                   : "r"((ex_ld ^ 16u) + (unsigned)(plane * 1024))
+                   : "memory");
+      return ((u0.x + u0.y) + (u0.z + u0.w)) + ((u1.x + u1.y) + (u1.z + u1.w));
+    };
     float q[KT];
-    float n2 = 0.f;
-    {
-      float sum[4 * NPL];
 #pragma unroll
-      for (int k = 0; k < 4 * NPL; ++k) sum[k] = 0.f;
-#pragma unroll
-      for (int gg = 0; gg < L; ++gg) {  // rows in order: a fixed summation order per frame
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) {
-          float4 v;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                       : "r"((ex_ld ^ (unsigned)(gg << 4)) + (unsigned)(p * 4096))
-                       : "memory");
-          sum[4 * p] += v.x;
-          sum[4 * p + 1] += v.y;
-          sum[4 * p + 2] += v.z;
-          sum[4 * p + 3] += v.w;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < KT; ++k) q[k] = sum[k];
-      n2 = sum[KT];
-    }
+    for (int k = 0; k < KT; ++k) q[k] = (am & (1u << k)) ? row_sum(k) : 1.f;  // inactive: any positive value, ck = -inf
+    const float n2 = row_sum(KT);
     // Unit normalisation y/(|y|+1e-10) (wpe.hpp:135): see cacgmm_pass2.cuh; only the floor and the likelihood see it
     float nr2 = 1.f;
     if (normalize) {
@@ -250,7 +250,6 @@ __global__ void __launch_bounds__(kEm3Threads, 1) em_pass3_kernel(EmPassArgs a) 
     }
     const float qfloor = kQuadFloor * nr2;
     const float* ckp = s_ck + pid * KTP;
-    const unsigned am = __reduce_or_sync(0xffffffffu, (unsigned)s_amask[pid]);
     float u[KT];
     float mx = -CUDART_INF_F;
 #pragma unroll

@@ -135,10 +135,10 @@ constexpr int em_lanes(int M, int KT) {
   if (M <= 4) return 2;
   if (M == 5) return KT <= 5 ? 2 : 4;
   if (M == 6) return 4;
-  if (M == 7) return KT <= 6 ? 4 : 8;
-  // M = 8: with 4 lanes the 16 K accumulators + two groups of frames go past 128 registers. The 8-lane shapes run
-  // the row-owner sweep (cacgmm_pass3.cuh): measured 20.4 ms against 21.1 ms for the two-phase sweep per 16-segment
-  // cfg3 step; at M = 7 the eighth lane of every frame would idle and the two-phase sweep wins (15.4 vs 16.7 ms, cfg2)
+  // M = 7, 8 run the row-owner sweep (cacgmm_pass3.cuh), one row of the outer product per lane: 8 lanes per frame
+  // (at M = 7 the eighth lane of a frame idles; still 14.9 vs 15.4 ms per cfg2 step against the two-phase sweep once
+  // the inactive classes are skipped). M = 8 with K <= 3 keeps 4 lanes and the two-phase sweep.
+  if (M == 7) return 8;
   return KT <= 3 ? 4 : 8;
 }
 /// Class count the kernels are instantiated for (>= K).
