@@ -419,6 +419,9 @@ def run_ours(args, rank, world, local_rank):
                                     else k.get("peak_note", b.peak_src)),
                     "avg_launch_ms": round(k["ms_per_step"] / max(1, k["launches_per_step"]), 4),
                     "share_of_step": round(k["ms_per_step"] / (r["ms_profiled"] / args.steps), 4),
+                    "note": ("algorithmic flops are SURVEY 8(d)'s count, which charges all K classes per frame; the sweep "
+                             "skips classes that are inactive in a whole group of 32 frames, so the executed FMA count is "
+                             "lower (DESIGN.md section 3)") if top == "em_pass" else None,
                     "timing": "CUDA events around every launch of a second pass of the same K steps "
                               "(%.3f ms/step with the events in; the headline pass has none)"
                               % (r["ms_profiled"] / args.steps)}

@@ -406,19 +406,25 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
     d.mask_off = (long long)h_masks.size();
     // activity rows -> pattern ids (first-appearance order) + class bit masks
     if (s.activity != nullptr) {
-      std::map<uint32_t, int> seen;
-      for (int t = 0; t < s.T; ++t) {
+      // K <= 8 classes: a row is one of at most 256 bit masks, so the id table is a flat array
+      int id_of[256];
+      std::fill(id_of, id_of + 256, -1);
+      int nseen = 0;
+      const size_t base = h_pat.size();
+      h_pat.resize(base + (size_t)s.T);
+      unsigned char* out_ids = h_pat.data() + base;
+      const uint8_t* act = s.activity;
+      for (int t = 0; t < s.T; ++t, act += s.K) {
         uint32_t m = 0;
-        for (int k = 0; k < s.K; ++k)
-          if (s.activity[(size_t)t * s.K + k]) m |= 1u << k;
-        auto it = seen.find(m);
-        if (it == seen.end()) {
-          it = seen.emplace(m, (int)seen.size()).first;
+        for (int k = 0; k < s.K; ++k) m |= (act[k] ? 1u : 0u) << k;
+        int id = id_of[m];
+        if (id < 0) {
+          id = id_of[m] = nseen++;
           h_masks.push_back(m);
         }
-        h_pat.push_back((unsigned char)it->second);
+        out_ids[t] = (unsigned char)id;
       }
-      d.npat = (int)seen.size();
+      d.npat = nseen;
     } else {
       d.npat = 0;
     }
