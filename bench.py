@@ -241,14 +241,16 @@ class Bench:
             self.dist.barrier()
         self.torch.cuda.synchronize()
 
+    device = "cuda"  # the CPU test of the aggregation (gloo, world size 2) overrides it
+
     def max_over_ranks(self, values):
-        t = self.torch.tensor(values, dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor(values, dtype=self.torch.float64, device=self.device)
         if self.world > 1:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return [float(v) for v in t]
 
     def sum_over_ranks(self, values):
-        t = self.torch.tensor(values, dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor(values, dtype=self.torch.float64, device=self.device)
         if self.world > 1:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return [float(v) for v in t]

@@ -162,3 +162,63 @@ def test_reference_arm_prints_one_json_line_on_cpu():
     assert d["gpu_launches"] == 0 and d["value"] > 0 and d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["name"] == "tiny" and d["config"]["segments_per_gpu"] == 2
+
+
+def _agg_worker(rank, world, port, q):
+    """One rank of the bench's aggregation: its own timings in, whole-job numbers out (gloo on CPU)."""
+    import importlib.util
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("gss_bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+
+    class Part:
+        def __init__(self, b, e):
+            self.sample_begin, self.sample_end = b, e
+
+    class Audio:
+        def num_samples(self):
+            return 640000
+
+    class Seg:
+        def __init__(self):
+            self.parts, self.audio = [Part(240000, 400000)], Audio()   # 10 s cut out of a 40 s window
+
+    b = bench.Bench.__new__(bench.Bench)   # no device, no library: only the reduction logic is under test
+    b.torch, b.dist, b.rank, b.world, b.device = torch, dist, rank, world, "cpu"
+    nseg = 4 if rank == 0 else 2           # uneven shards, as the size-balanced partition of the sweep produces
+    calls = [(None, [Seg() for _ in range(nseg)])]
+    r = {"ms": 100.0 if rank == 0 else 80.0, "e2e_ms": 120.0 if rank == 0 else 90.0, "h2d": 1000 * nseg, "d2h": 10 * nseg,
+         "launches": 7}
+    q.put((rank, bench.summarise(b, calls, r, steps=2, scaling="strong")))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_aggregates_ranks_as_sum_of_work_over_slowest_rank():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_agg_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=180) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        d = got[rank]
+        assert d["segments"] == 6 and d["scaling"] == "strong"
+        assert d["ms_per_step"] == 50.0                                 # slowest rank: 100 ms over 2 steps
+        assert d["value"] == pytest.approx(6 * 10.0 * 2 / 0.100)        # 60 s of output per step, both ranks' work
+        assert d["xrt_processed"] == pytest.approx(6 * 40.0 * 2 / 0.100)
+        assert d["e2e"]["value"] == pytest.approx(6 * 10.0 * 2 / 0.120) and d["e2e"]["ms_per_step"] == 60.0
+        assert d["e2e"]["h2d_bytes_per_step"] == 6000 and d["e2e"]["d2h_bytes_per_step"] == 60
+        assert d["gpu_launches"] == 14 and d["per_rank_ms_per_step"] == [50.0, 40.0]
