@@ -136,23 +136,27 @@ def algorithmic_work(segs, cfg):
     w = {k: {"flops": 0.0, "bytes": 0.0} for k in ("stft", "wpe_power", "wpe_gram", "wpe_solve", "wpe_apply", "em_pass",
                                                    "em_update", "mvdr", "apply", "istft")}
     import math
+    # which WPE kernels a segment runs (api.cu: by shape unless GSS_B200_WPE_GRAM / _APPLY force one)
+    g_env, a_env = os.environ.get("GSS_B200_WPE_GRAM", "auto"), os.environ.get("GSS_B200_WPE_APPLY", "auto")
     for ss in segs:
         M, N = ss.audio.channels.shape
         T, K = ss.activity.grid.shape
         FT = F * T
         km = cfg.wpe.taps * M
+        tc_gram = g_env == "tc" or (g_env != "fp32" and M >= 3)
+        tc_apply = a_env == "tc" or (a_env != "fp32" and M >= 5)
         w["stft"]["bytes"] += 4 * M * N + 8 * FT * M
         w["stft"]["flops"] += M * T * (2.5 * n * math.log2(n) + n)
         if J:
             # with psd_context 0 the tensor-core prediction writes the next iteration's weights: one power pass
-            n_power = 1 if (cfg.wpe.psd_context == 0 and os.environ.get("GSS_B200_WPE_APPLY") != "fp32") else J
+            n_power = 1 if (cfg.wpe.psd_context == 0 and tc_apply) else J
             w["wpe_power"]["bytes"] += n_power * (8 * FT * M + 4 * FT)
             w["wpe_gram"]["flops"] += J * FT * 8 * (km * (km + 1) / 2 + km * M)
             w["wpe_gram"]["bytes"] += J * (8 * FT * M + 4 * FT)
             w["wpe_solve"]["flops"] += J * F * (8 / 3 * km ** 3 + 16 * km * km * M)
             w["wpe_apply"]["flops"] += J * FT * 8 * km * M
             w["wpe_apply"]["bytes"] += J * 2 * 8 * FT * M
-        if J:
+        if J and tc_gram:
             # tensor-core Gram: executed TF32 flops (3xTF32 split; a 128 x NR accumulator plus the corner block as
             # an M = 64 MMA of N2 columns; the tensor core's cost floor is that of M = 128 for either)
             kmp = (km + 7) // 8 * 8
@@ -160,6 +164,7 @@ def algorithmic_work(segs, cfg):
             n2 = max(0, nr - 128)
             w["wpe_gram"]["tensor_flops"] = (w["wpe_gram"].get("tensor_flops", 0.0) +
                                              J * FT * 3 * 2 * (128 * nr + 64 * n2))
+        if J and tc_apply:
             # tensor-core prediction: per frame and tap 2 k-steps of 8, A_hi x [B_hi | B_lo] (N = 32) + A_lo x B_hi (N = 16)
             w["wpe_apply"]["tensor_flops"] = w["wpe_apply"].get("tensor_flops", 0.0) + J * FT * cfg.wpe.taps * 2 * 2 * 8 * 48
         w["em_pass"]["flops"] += (I + 1) * FT * (3 * M * M + 4 * M * M * K + 20 * K)
@@ -185,8 +190,7 @@ def sum_work(calls):
 
 def kernel_table(kms, steps, work, nseg, hbm_peak, tf32_peak, fp32_peak, peak_src, traffic):
     """Per kernel class: ms per step, launches, the roofline that bounds it and the fraction reached."""
-    tc_gram = os.environ.get("GSS_B200_WPE_GRAM", "tc") != "fp32"
-    tc_apply = os.environ.get("GSS_B200_WPE_APPLY", "tc") != "fp32"
+    tc_gram = tc_apply = True  # a class is tensor-bound when any of its segments ran the tcgen05 kernel (tensor_flops > 0)
     kernels = {}
     for name, (kms_total, n) in kms.items():
         if n == 0 or name not in work:

@@ -73,8 +73,12 @@ struct gss_b200_ctx {
   std::vector<ProfRec> prof_recs;
   double kernel_ms[GSS_B200_NUM_KERNELS] = {0};
   long long kernel_launches[GSS_B200_NUM_KERNELS] = {0};
-  int wpe_gram_tc = 1;       // GSS_B200_WPE_GRAM=fp32 selects the FP32-FMA Gram kernel instead of tcgen05
-  int wpe_apply_tc = 1;      // GSS_B200_WPE_APPLY=fp32 selects the FP32-FMA prediction kernel instead of tcgen05
+  // WPE kernel choice: 2 = by shape (default), 1 = tcgen05 wherever it is supported (GSS_B200_WPE_GRAM / _APPLY = tc),
+  // 0 = the FP32-FMA kernels (= fp32). By shape: the 128-row MMA tiles pay off from 3 channels (Gram) / 5 channels
+  // (prediction) upwards; below that the FP32 kernels win (tools/shape_bench.py: prediction 0.78 vs 3.18 ms at M = 2,
+  // 1.98 vs 3.21 at M = 4, 3.02 vs 3.32 at M = 5; Gram 6.85 vs 8.46 ms at M = 2, 16.9 vs 9.4 at M = 4).
+  int wpe_gram_tc = 2;
+  int wpe_apply_tc = 2;
   int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
   int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
   // Shape groups of one batch (segments sharing channel count and class tier) are independent: they are enqueued
@@ -510,7 +514,7 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
   }
   if (need.wpe) {
     g.w = m.get<float>(o_w);
-    g.use_tc = c->wpe_gram_tc && wpe_tc_supported(km, M) && g.max_wchunks == 1;
+    g.use_tc = (c->wpe_gram_tc == 1 || (c->wpe_gram_tc == 2 && M >= 3)) && wpe_tc_supported(km, M) && g.max_wchunks == 1;
     if (g.use_tc)
       g.gram_raw = m.get<float>((size_t)o_f * wpe_tc_cell_floats(km, M));
     else
@@ -561,7 +565,8 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first
   a.gram = g.gram;
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
-  a.apply_tc = c->wpe_apply_tc && wpe_apply_tc_supported(w.taps, w.delay, g.M);
+  a.apply_tc = (c->wpe_apply_tc == 1 || (c->wpe_apply_tc == 2 && g.M >= 5)) &&
+               wpe_apply_tc_supported(w.taps, w.delay, g.M);
   a.debug_rp = nullptr;
   a.w_next = nullptr;
   a.fb_scratch = g.fb_scratch;
@@ -810,8 +815,8 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
     unsigned long long thr = ~0ull;  // keep freed blocks cached for the next batch
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  if (const char* s = std::getenv("GSS_B200_WPE_GRAM")) c->wpe_gram_tc = std::strcmp(s, "fp32") != 0;
-  if (const char* s = std::getenv("GSS_B200_WPE_APPLY")) c->wpe_apply_tc = std::strcmp(s, "fp32") != 0;
+  if (const char* s = std::getenv("GSS_B200_WPE_GRAM")) c->wpe_gram_tc = std::strcmp(s, "fp32") == 0 ? 0 : std::strcmp(s, "tc") == 0 ? 1 : 2;
+  if (const char* s = std::getenv("GSS_B200_WPE_APPLY")) c->wpe_apply_tc = std::strcmp(s, "fp32") == 0 ? 0 : std::strcmp(s, "tc") == 0 ? 1 : 2;
   if (const char* s = std::getenv("GSS_B200_EM_CHUNK_FRAMES")) c->em_chunk_frames = std::atoi(s);
   if (const char* s = std::getenv("GSS_B200_WPE_CHUNK_FRAMES")) c->wpe_chunk_frames = std::atoi(s);
   if (const char* s = std::getenv("GSS_B200_WAVES")) c->waves = std::max(1, std::atoi(s));

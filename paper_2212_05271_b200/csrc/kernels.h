@@ -134,12 +134,11 @@ constexpr int em_lanes(int M, int KT) {
   if (M == 1) return 1;
   if (M <= 4) return 2;
   if (M == 5) return KT <= 5 ? 2 : 4;
-  if (M == 6) return 4;
+  if (M == 6) return 4;  // (the row-owner sweep with two idle lanes per frame: 13.0 vs 11.7 ms, tools/shape_bench.py 6 2)
   // M = 7, 8 run the row-owner sweep (cacgmm_pass3.cuh), one row of the outer product per lane: 8 lanes per frame
   // (at M = 7 the eighth lane of a frame idles; still 14.9 vs 15.4 ms per cfg2 step against the two-phase sweep once
-  // the inactive classes are skipped). M = 8 with K <= 3 keeps 4 lanes and the two-phase sweep.
-  if (M == 7) return 8;
-  return KT <= 3 ? 4 : 8;
+  // the inactive classes are skipped; at M = 8 it wins for every class count: 14.5 vs 17.1 ms at K = 3).
+  return 8;
 }
 /// Class count the kernels are instantiated for (>= K).
 constexpr int em_class_tier(int K) { return K <= 2 ? 2 : K <= 3 ? 3 : K <= 4 ? 4 : K <= 5 ? 5 : K <= 6 ? 6 : 8; }
