@@ -338,3 +338,16 @@ def test_enhance_sweep_shapes_channels_and_iterations(gss, oracle, simd_oracle, 
     # ll_final sums every bin, the unstable ones included: gated only when there are none
     check_segment(gss, oracle, simd_oracle, ss, cfg, f"sweep M={channels} S={speakers} I={iterations}", max_abs=2e-2,
                   max_unstable=cap, ll_gate_unstable=None)
+
+
+@pytest.mark.parametrize("channels,speakers", [(7, 1), (7, 4), (7, 5), (8, 1), (8, 2), (8, 5), (8, 7)])
+def test_enhance_row_owner_sweep_every_class_tier(gss, oracle, simd_oracle, channels, speakers):
+    # the row-owner EM sweep serves every 7- and 8-channel shape; its last-sweep flavour (MVDR statistics fused) is only
+    # reachable through enhance_batch: class tiers 2, 3, 5, 6, 8 on short segments (K = speakers + noise)
+    import synthbench as synth
+    from paper_2212_05271_b200.gss import scheduler, stft, wpe
+    cfg = scheduler.PipelineConfig(stft.StftConfig(512, 128, 0, 16000), wpe.WpeConfig(6, 2, 2, 0, 1e-10), True, 6)
+    ss = synth.make_supersegment(7100 + 10 * channels + speakers, channels, speakers, 3.0, 2.0, cfg)
+    assert ss.activity.grid.shape[1] == speakers + 1
+    check_segment(gss, oracle, simd_oracle, ss, cfg, f"row-owner M={channels} K={speakers + 1}", max_abs=2e-2,
+                  max_unstable=0.05, ll_gate_unstable=None)

@@ -237,7 +237,10 @@ def _em_problem(seed, f, t, m, k, noise=True):
 
 @pytest.mark.parametrize("m,k,noise", [(4, 3, True), (7, 3, True), (7, 4, True), (8, 5, True), (2, 2, True),
                                        (3, 2, False), (5, 4, True), (6, 6, True), (8, 7, True), (1, 2, True),
-                                       (7, 8, True), (5, 6, False)])
+                                       (7, 8, True), (5, 6, False),
+                                       # every class tier of the row-owner sweep (cacgmm_pass3.cuh: M = 7, 8)
+                                       (7, 2, True), (7, 5, True), (7, 6, False), (8, 2, True), (8, 3, True), (8, 4, False),
+                                       (8, 6, True), (8, 8, True)])
 def test_em_fit_matches_oracle(gss, oracle, m, k, noise):
     f, t, iters = 6, 520, 8
     y, act = _em_problem(100 * m + k, f, t, m, k, noise)
