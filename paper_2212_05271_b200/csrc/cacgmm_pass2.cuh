@@ -53,8 +53,14 @@ struct EmPass2Cfg {
   /// does it. SPW = 4 (L = 8): a quarter-warp is 4 frames x 2 slices whose chunk numbers differ in bit 1 (CPG = 2),
   /// so the frame's bit 1 must land elsewhere: bits (0, 1, 2) -> (0, 2, 1). With the identity these loads were
   /// 2-way conflicted (41 M conflict cycles per cfg3 sweep).
+  static constexpr int FPL = NCHP < 8 ? 8 / NCHP : 1;  // frames per 128-byte line of a narrow scratch
   __host__ __device__ static constexpr unsigned swz(unsigned fr) {
-    return (L == 8 && NDOFP == 8 ? ((fr & 1u) | ((fr & 2u) << 1) | ((fr & 4u) >> 1) | (fr & ~7u)) : fr) & (unsigned)(NCHP - 1);
+    if (L == 8 && NDOFP == 8) return ((fr & 1u) | ((fr & 2u) << 1) | ((fr & 4u) >> 1) | (fr & ~7u)) & (unsigned)(NCHP - 1);
+    // narrow scratch rows (NCHP < 8: M <= 4): 8 / NCHP frames share one 128-byte line, and the 8 frames of a
+    // quarter-warp must land in 8 different 16-byte columns of it, so the XOR term advances once per line, not
+    // once per frame (with fr % NCHP, frames fr and fr + NCHP collided: 29 % excess wavefronts at M = 4)
+    if (NCHP < 8) return (fr / (unsigned)FPL) & (unsigned)(NCHP - 1);
+    return fr & (unsigned)(NCHP - 1);
   }
   static constexpr int NW = kEmThreads / 32;
   // coefficient table of one lane slice: [dof][class] packed (no class padding), rounded up to whole float4s
