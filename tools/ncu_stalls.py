@@ -59,6 +59,12 @@ def main():
     print("  opcode mix: " + ", ".join("%s %.1f%% (%.1f%% of samples)" % (o, 100 * c / ins, 100 * ms[o] / smp) for o, c in mix.most_common(10)))
     print("  shared wavefronts: %d, excessive (bank conflicts): %d" % (
         sum(num(r[ix["L1 Wavefronts Shared"]]) for r in data), sum(num(r[ix["L1 Wavefronts Shared Excessive"]]) for r in data)))
+    print("  most excessive shared wavefronts:")
+    for r in sorted(data, key=lambda r: -num(r[ix["L1 Wavefronts Shared Excessive"]]))[:6]:
+        if num(r[ix["L1 Wavefronts Shared Excessive"]]) > 0:
+            print("    %10d of %10d  %s" % (num(r[ix["L1 Wavefronts Shared Excessive"]]), num(r[ix["L1 Wavefronts Shared"]]),
+                                            r[ix["Source"]][:60]))
+    print("  most sampled instructions:")
     for r in sorted(data, key=lambda r: -num(r[ix["# Samples"]]))[:12]:
         print("    %6d  %-60s short_sb %s mio %s long_sb %s" % (num(r[ix["# Samples"]]), r[ix["Source"]][:60], r[ix["stall_short_sb"]],
                                                                  r[ix["stall_mio"]], r[ix["stall_long_sb"]]))
