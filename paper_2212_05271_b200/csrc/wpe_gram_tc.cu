@@ -258,7 +258,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     static_assert(kTcWorkerWarps == kKCores, "one worker warp per K chunk");
     const int k = warp * 4 + (lane & 3), r8 = lane >> 2;
     const int word0 = warp * kCoreWords + lane;  // core (rg, kc = warp) -> (rg * kKCores + warp) * 32 + lane
-    const int nrg_a = KMP / 8, nrg = NB / 8;
+    // row groups that carry data: [Re a | Im a | Re y | Im y]; the groups after them (padding up to NB rows: a third
+    // of the 128-row tile at M = 4) are zero in every chunk, so they are zeroed once here and never rewritten
+    const int nrg_a = KMP / 8, nrg = 2 * nrg_a + 2;
+    for (int i = tid; i < 4 * (NB - 8 * nrg) * kKC; i += kTcWorkers) {
+      const int per = (NB - 8 * nrg) * kKC;  // zero words per operand buffer
+      opbuf[(size_t)(i / per) * buf_words + (size_t)(8 * nrg) * kKC + (i % per)] = 0.f;
+    }
 
     issue_slab(0);
     for (int c = 0; c < nchunk; ++c) {
