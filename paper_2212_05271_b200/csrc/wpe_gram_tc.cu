@@ -40,6 +40,21 @@ __host__ __device__ inline int tc_rows(int km, int M) { return ((2 * tc_kmp(km) 
 __host__ __device__ inline int tc_buf_rows(int km, int M) { return tc_rows(km, M) < 128 ? 128 : tc_rows(km, M); }
 __host__ __device__ inline int tc_n2(int km, int M) { return tc_rows(km, M) > 128 ? tc_rows(km, M) - 128 : 0; }
 __host__ __device__ inline int tc_cols(int km, int M) { return tc_rows(km, M) + tc_n2(km, M); }         // D1 | D2
+/// Bytes ahead of the operand buffers: barriers, Gram weights, three stages of planar slabs (H = history frames).
+__host__ __device__ inline size_t tc_head_bytes(int M, int H) {
+  const size_t off = 128 + sizeof(float) * (3 * kKC + 6 * (size_t)(kKC + H + kLook) * M);
+  return (off + 127) & ~(size_t)127;
+}
+__host__ __device__ inline size_t tc_smem_bytes(int km, int M, int H, int stages) {
+  return tc_head_bytes(M, H) + sizeof(float) * 2 * (size_t)stages * (size_t)tc_buf_rows(km, M) * kKC;
+}
+/// Operand / accumulator pipeline depth. With two stages the tensor core idles while the workers drain and refill
+/// the buffer it just finished, which at the small tiles takes longer than a chunk of MMAs (M = 4: 1685 cycles of
+/// MMAs against ~3700 of drain + expansion per 64-frame chunk). Three stages fit when the tile is 128 rows, an
+/// accumulator set is at most 160 columns and the slabs leave room (M = 4, 5 at the default history: 196 KB of operands).
+__host__ __device__ inline int tc_stages(int km, int M, int H) {
+  return tc_buf_rows(km, M) == 128 && tc_cols(km, M) <= 160 && tc_smem_bytes(km, M, H, 3) <= 224 * 1024 ? 3 : 2;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -73,18 +88,23 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a_desc, uint6
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+/// Bounded wait: a protocol error traps (an error for the caller) instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@p bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+  const uint32_t addr = smem_u32(bar);
+  for (int spin = 0; spin < (1 << 28); ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+  }
+  __trap();
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -117,25 +137,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   const int SF = kKC + H + kLook;  // slab frames per chunk
 
   // shared memory carve-up
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);             // [2] operands of a chunk are staged
-  uint64_t* done = full + 2;                                          // [2] MMAs of a chunk are complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + 32);
+  const int NS = tc_stages(km, M, H);                                    // operand buffers / accumulator sets
+  const uint32_t setw = NS == 3 ? 160u : 256u;                        // tensor-memory columns per accumulator set
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);             // [3] operands of a chunk are staged
+  uint64_t* done = full + 3;                                          // [3] MMAs of a chunk are complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + 64);
   float* wbuf = reinterpret_cast<float*>(smem_raw + 128);             // [3][kKC] Gram weights
   float* planes = wbuf + 3 * kKC;                                     // [3 stages][re, im][SF * M]
   const int plane_words = SF * M;
-  size_t off = 128 + sizeof(float) * (3 * kKC + 6 * (size_t)plane_words);
-  off = (off + 127) & ~(size_t)127;
+  const size_t off = tc_head_bytes(M, H);
   const int buf_words = NB * kKC;                                     // one operand buffer (hi or lo)
   float* opbuf = reinterpret_cast<float*>(smem_raw + off);            // [stage][hi/lo][buf_words]
 
   if (tid == 0) {
-    mbar_init(&full[0], kTcWorkerWarps);
-    mbar_init(&full[1], kTcWorkerWarps);
-    mbar_init(&done[0], 1);
-    mbar_init(&done[1], 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&full[i], kTcWorkerWarps);
+      mbar_init(&done[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // Two accumulator sets (D1 | D2 each): every chunk's products start from zero and are folded into FP32
+  // NS accumulator sets (D1 | D2 each): every chunk's products start from zero and are folded into FP32
   // registers with round-to-nearest. The tensor core's own accumulation truncates; a chain of thousands
   // of MMAs loses ~1e-4 of the Gram, a chain of 12 stays at the 3xTF32 level (1e-6).
   if (warp == kTcWorkerWarps) {
@@ -156,11 +177,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     if (lane == 0) {
       const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16, 64);
       for (int c = 0; c < nchunk; ++c) {
-        const int b = c & 1;
-        mbar_wait(&full[b], (uint32_t)((c / 2) & 1));
+        const int b = c % NS;
+        mbar_wait(&full[b], (uint32_t)((c / NS) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t a_hi = smem_u32(opbuf + (size_t)(2 * b) * buf_words), a_lo = a_hi + 4u * (uint32_t)buf_words;
-        const uint32_t d1 = tmem_base + (uint32_t)(b * 256), d2 = d1 + (uint32_t)NR;
+        const uint32_t d1 = tmem_base + (uint32_t)b * setw, d2 = d1 + (uint32_t)NR;
 #pragma unroll
         for (int ks = 0; ks < kKC / 8; ++ks) {
           const uint32_t accf = ks > 0 ? 1u : 0u;  // every chunk starts its accumulator set from zero
@@ -226,7 +247,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     const int q = warp & 3, qcol = (warp >> 2) * NCQ;
 
     auto drain = [&](int set) {
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(set * 256 + qcol);
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)set * setw + (uint32_t)qcol;
       constexpr int kBatch = 32;  // columns in flight per wait
 #pragma unroll
       for (int b0 = 0; b0 < kAccPerThread; b0 += kBatch) {
@@ -261,14 +282,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     // row groups that carry data: [Re a | Im a | Re y | Im y]; the groups after them (padding up to NB rows: a third
     // of the 128-row tile at M = 4) are zero in every chunk, so they are zeroed once here and never rewritten
     const int nrg_a = KMP / 8, nrg = 2 * nrg_a + 2;
-    for (int i = tid; i < 4 * (NB - 8 * nrg) * kKC; i += kTcWorkers) {
+    for (int i = tid; i < 2 * NS * (NB - 8 * nrg) * kKC; i += kTcWorkers) {
       const int per = (NB - 8 * nrg) * kKC;  // zero words per operand buffer
       opbuf[(size_t)(i / per) * buf_words + (size_t)(8 * nrg) * kKC + (i % per)] = 0.f;
     }
 
     issue_slab(0);
     for (int c = 0; c < nchunk; ++c) {
-      const int b = c & 1, st = c % 3;
+      const int b = c % NS, st = c % 3;
       if (c + 1 < nchunk) {
         issue_slab(c + 1);  // stage (c+1)%3 was last read by the expansion of chunk c-2
         asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -276,9 +297,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       workers_sync();  // slab of chunk c has landed for every worker
-      if (c >= 2) {
-        // MMAs of chunk c-2 are complete: operand buffer b and accumulator set b are ours again
-        mbar_wait(&done[b], (uint32_t)((c / 2 - 1) & 1));
+      if (c >= NS) {
+        // MMAs of chunk c - NS are complete: operand buffer b and accumulator set b are ours again
+        mbar_wait(&done[b], (uint32_t)((c / NS - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         drain(b);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -293,6 +314,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
 #pragma unroll
       for (int rg = 0; rg < 24; ++rg) {  // NB <= 192 rows
         if (rg < nrg) {
+          // (loading every row group's value ahead of the stores was measured: 8.74 against 8.32 ms at M = 4)
           float v;
           if (rg < nrg_a) v = rk[rg * 8];                              // Re a: element rg*8 + r8 of the window
           else if (rg < 2 * nrg_a) v = ik[(rg - nrg_a) * 8];           // Im a
@@ -309,11 +331,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[b]);
     }
-    // fold in the last two chunks
-    for (int c = max(0, nchunk - 2); c < nchunk; ++c) {
-      mbar_wait(&done[c & 1], (uint32_t)((c / 2) & 1));
+    // fold in the last NS chunks
+    for (int c = max(0, nchunk - NS); c < nchunk; ++c) {
+      mbar_wait(&done[c % NS], (uint32_t)((c / NS) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      drain(c & 1);
+      drain(c % NS);
     }
     float* out = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT) +
                  (long long)(q * 32 + lane) * NCT + qcol;
@@ -341,9 +363,7 @@ int wpe_tc_rows(int km, int M) { return tc_rows(km, M); }
 template <int M>
 static cudaError_t launch_tc_m(const WpeArgs& a, int nseg, int F, cudaStream_t st) {
   const int km = a.taps * M, H = a.delay + a.taps - 1;
-  size_t off = 128 + sizeof(float) * (3 * kKC + 6 * (size_t)(kKC + H + kLook) * M);
-  off = (off + 127) & ~(size_t)127;
-  size_t smem = off + sizeof(float) * 4 * (size_t)tc_buf_rows(km, M) * kKC;
+  size_t smem = tc_smem_bytes(km, M, H, tc_stages(km, M, H));
   if (smem > 224 * 1024) return cudaErrorInvalidConfiguration;
   // all 512 tensor-memory columns belong to one CTA: keep a second CTA off the SM
   smem = std::max<size_t>(smem, 120 * 1024);
