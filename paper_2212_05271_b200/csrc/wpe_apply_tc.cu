@@ -26,6 +26,9 @@ namespace {
 constexpr int kTile = 128;                 // frames per MMA tile (the MMA's M)
 constexpr int kAppThreads = 160;           // 1 issuer warp + 4 worker warps
 constexpr int kKPad = 16;                  // K per tap: 2 M floats padded to 16
+#ifndef GSS_APPLY_3BLOCK_FROM
+#define GSS_APPLY_3BLOCK_FROM 8
+#endif
 constexpr int kNOut = 16;                  // N: [Re out (8) | Im out (8)]
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -84,12 +87,18 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 }
 __device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xffffe000u); }
 
-__host__ __device__ inline int app_rows(int H) { return kTile + ((H + 7) & ~7); }  // staged slab rows per tile
+// Staged slab rows per tile: exactly the 128 frames and their H history rows. (Not rounded up to the 8-row core
+// matrix: the MMA of tap u reads rows u .. u + 127, and the 1 KB this saves is what lets four blocks share an SM.)
+__host__ __device__ inline int app_rows(int H) { return kTile + H; }
+// Blocks per SM the register allocation aims at. Four hide more of a tile's load -> stage -> MMA -> store latency
+// (M = 5: 3.32 -> 3.09 ms, M = 6: 3.39 -> 3.19 ms per 16-segment step); at M = 8 the serial MMA stream of the SM's one
+// tensor pipe is what binds and the fourth block only adds contention (4.39 -> 4.76 ms), so it keeps three.
+__host__ __device__ constexpr int app_min_blocks(int M) { return M >= GSS_APPLY_3BLOCK_FROM ? 3 : 4; }
 
 }  // namespace
 
 template <int M>
-__global__ void __launch_bounds__(kAppThreads) wpe_apply_tc_kernel(WpeArgs a) {
+__global__ void __launch_bounds__(kAppThreads, app_min_blocks(M)) wpe_apply_tc_kernel(WpeArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const SegDev sd = a.segs[blockIdx.y];
   if (!sd.wpe_active) return;
