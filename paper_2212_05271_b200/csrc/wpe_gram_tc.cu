@@ -176,6 +176,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     // ===== MMA issuer =====
     if (lane == 0) {
       const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16, 64);
+      // The corner (rows and columns >= 128) is read back only where an Im a row lies beyond row 127, i.e. when
+      // KMP + km > 128 (M = 7, 8). At M = 6 rows 128.. are the y rows, needed as columns only: no corner MMAs, and
+      // since every MMA costs ~150 cycles whatever its shape (tools/mma_probe.cu) that is half of the MMA stream.
+      const bool corner = N2 > 0 && KMP + km > 128;
       for (int c = 0; c < nchunk; ++c) {
         const int b = c % NS;
         mbar_wait(&full[b], (uint32_t)((c / NS) & 1));
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
           mma_tf32(d1, dh, dh, idesc1, accf);
           mma_tf32(d1, dh, dl, idesc1, 1u);
           mma_tf32(d1, dl, dh, idesc1, 1u);
-          if (N2 > 0) {
+          if (corner) {
             // the corner is an M = 64 MMA on the last 64 rows: the kernel is bound by the operand bytes it
             // streams from shared memory, and a 64-row A tile is half of them (row r of that accumulator
             // lives in tensor-memory lane 32 (r / 16) + r % 16)
