@@ -78,6 +78,7 @@ struct gss_b200_ctx {
   // (prediction) upwards; below that the FP32 kernels win (tools/shape_bench.py: prediction 0.78 vs 3.18 ms at M = 2,
   // 1.98 vs 3.21 at M = 4, 3.02 vs 3.32 at M = 5; Gram 6.85 vs 8.46 ms at M = 2, 16.9 vs 9.4 at M = 4).
   int wpe_gram_tc = 2;
+  int wpe_gram_f16 = 1;      // tensor-core Gram operand split: 1 = FP16 (K = 16 per MMA), 0 = TF32 (GSS_B200_WPE_GRAM_KIND = tf32)
   int wpe_apply_tc = 2;
   int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
   int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
@@ -565,6 +566,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first
   a.gram = g.gram;
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
+  a.gram_f16 = c->wpe_gram_f16;
   a.apply_tc = (c->wpe_apply_tc == 1 || (c->wpe_apply_tc == 2 && g.M >= 5)) &&
                wpe_apply_tc_supported(w.taps, w.delay, g.M);
   a.debug_rp = nullptr;
@@ -816,6 +818,7 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (const char* s = std::getenv("GSS_B200_WPE_GRAM")) c->wpe_gram_tc = std::strcmp(s, "fp32") == 0 ? 0 : std::strcmp(s, "tc") == 0 ? 1 : 2;
+  if (const char* s = std::getenv("GSS_B200_WPE_GRAM_KIND")) c->wpe_gram_f16 = std::strcmp(s, "tf32") == 0 ? 0 : 1;
   if (const char* s = std::getenv("GSS_B200_WPE_APPLY")) c->wpe_apply_tc = std::strcmp(s, "fp32") == 0 ? 0 : std::strcmp(s, "tc") == 0 ? 1 : 2;
   if (const char* s = std::getenv("GSS_B200_EM_CHUNK_FRAMES")) c->em_chunk_frames = std::atoi(s);
   if (const char* s = std::getenv("GSS_B200_WPE_CHUNK_FRAMES")) c->wpe_chunk_frames = std::atoi(s);
@@ -1584,6 +1587,7 @@ gss_status gss_b200_debug_wpe_gram(gss_b200_ctx* c, const float* in, int32_t bin
   a.gram = g.gram;
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
+  a.gram_f16 = c->wpe_gram_f16;
   a.apply_tc = 0;
   a.w_next = nullptr;
   a.debug_rp = d_rp;

@@ -54,6 +54,7 @@ struct WpeArgs {
   int fb_slots;
   cdbl* debug_rp;       // non-null: the solve kernel only dumps hermitized R (km x km) and P (km x M) per bin
   int use_tc;           // 1: the Gram of this iteration came from wpe_gram_tc_kernel
+  int gram_f16;         // tensor-core Gram: 1 = FP16 hi / lo split (K = 16 per MMA), 0 = TF32 split (K = 8)
   int apply_tc;         // 1: the prediction runs on the tensor cores (wpe_apply_tc_kernel)
   float* w_next;        // tensor-core prediction only: also write the NEXT iteration's Gram weights (psd_context 0)
 };

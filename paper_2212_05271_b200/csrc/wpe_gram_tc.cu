@@ -18,6 +18,8 @@
 // buffer's mbarrier; the next chunk is expanded into the other buffer while the tensor core runs.
 #include <algorithm>
 
+#include <cuda_fp16.h>
+
 #include "kernels.h"
 
 namespace gssb {
@@ -27,9 +29,14 @@ namespace {
 constexpr int kTcWorkers = 512;             // 16 warps expand the operands and fold the accumulators
 constexpr int kTcWorkerWarps = kTcWorkers / 32;
 constexpr int kTcThreads = kTcWorkers + 32; // + one warp whose lane 0 issues the MMAs
-constexpr int kKC = 64;                     // frames per pipeline stage (8 MMA k-steps of 8) = 4 per worker warp
+constexpr int kKW = 64;                     // 32-bit words per operand row and pipeline stage: 8 MMA k-steps of 32 bytes
 constexpr int kCoreWords = 32;              // one core matrix: 8 rows x 16 bytes
-constexpr int kKCores = kKC / 4;            // core matrices along K per row group (= kTcWorkerWarps)
+constexpr int kKCores = kKW / 4;            // core matrices along K per row group (= kTcWorkerWarps)
+// Frames per pipeline stage. kind::tf32 takes K = 8 frames per MMA (4 per worker warp and stage), kind::f16 K = 16
+// (8 per warp): an MMA costs ~150 cycles whatever its shape or kind (tools/mma_probe.cu), so the FP16 split halves
+// the MMA stream per frame -- and the operand bytes, drains and barriers with it.
+__host__ __device__ constexpr int tc_kc(int f16) { return f16 ? 128 : 64; }
+constexpr int kHead = 384;                  // barriers, the tensor-memory slot, the scale reduction scratch
 constexpr int kLook = 8;                    // look-ahead frames read by the padded rows
 constexpr int kAccPerThread = 56;           // register accumulators per thread: NCT <= 224 columns / 4 quarters
 
@@ -41,19 +48,19 @@ __host__ __device__ inline int tc_buf_rows(int km, int M) { return tc_rows(km, M
 __host__ __device__ inline int tc_n2(int km, int M) { return tc_rows(km, M) > 128 ? tc_rows(km, M) - 128 : 0; }
 __host__ __device__ inline int tc_cols(int km, int M) { return tc_rows(km, M) + tc_n2(km, M); }         // D1 | D2
 /// Bytes ahead of the operand buffers: barriers, Gram weights, three stages of planar slabs (H = history frames).
-__host__ __device__ inline size_t tc_head_bytes(int M, int H) {
-  const size_t off = 128 + sizeof(float) * (3 * kKC + 6 * (size_t)(kKC + H + kLook) * M);
+__host__ __device__ inline size_t tc_head_bytes(int M, int H, int kc) {
+  const size_t off = kHead + sizeof(float) * (3 * kc + 6 * (size_t)(kc + H + kLook) * M);
   return (off + 127) & ~(size_t)127;
 }
-__host__ __device__ inline size_t tc_smem_bytes(int km, int M, int H, int stages) {
-  return tc_head_bytes(M, H) + sizeof(float) * 2 * (size_t)stages * (size_t)tc_buf_rows(km, M) * kKC;
+__host__ __device__ inline size_t tc_smem_bytes(int km, int M, int H, int stages, int kc) {
+  return tc_head_bytes(M, H, kc) + sizeof(float) * 2 * (size_t)stages * (size_t)tc_buf_rows(km, M) * kKW;
 }
 /// Operand / accumulator pipeline depth. With two stages the tensor core idles while the workers drain and refill
 /// the buffer it just finished, which at the small tiles takes longer than a chunk of MMAs (M = 4: 1685 cycles of
 /// MMAs against ~3700 of drain + expansion per 64-frame chunk). Three stages fit when the tile is 128 rows, an
 /// accumulator set is at most 160 columns and the slabs leave room (M = 4, 5 at the default history: 196 KB of operands).
-__host__ __device__ inline int tc_stages(int km, int M, int H) {
-  return tc_buf_rows(km, M) == 128 && tc_cols(km, M) <= 160 && tc_smem_bytes(km, M, H, 3) <= 224 * 1024 ? 3 : 2;
+__host__ __device__ inline int tc_stages(int km, int M, int H, int kc) {
+  return tc_buf_rows(km, M) == 128 && tc_cols(km, M) <= 160 && tc_smem_bytes(km, M, H, 3, kc) <= 224 * 1024 ? 3 : 2;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -71,6 +78,22 @@ __device__ __forceinline__ uint64_t make_smem_desc(uint32_t addr, uint32_t lbo_b
 /// kind::tf32, FP32 accumulate, both operands K-major, M = 128.
 __device__ __forceinline__ uint32_t make_idesc_tf32(int n, int m = 128) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+/// kind::f16 with FP16 operands (format 0), FP32 accumulate, both operands K-major.
+__device__ __forceinline__ uint32_t make_idesc_f16(int n, int m = 128) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -124,8 +147,13 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 
 /// TAPS > 0 fixes the tap count at compile time (all loops unroll, no guards); TAPS == 0 reads it from the
 /// arguments.
-template <int M, int TAPS>
+/// F16 = 1: kind::f16 on an FP16 hi / lo split of the operands scaled, per stage, by a power of two that puts the
+/// largest magnitude of the stage just under 2^15 (FP16 keeps 11 bits down to 2^-14 and a 2^-24 grid below that, a
+/// range of 2^39 in all; the accumulators are rescaled exactly when they are folded). Same products as the TF32
+/// split: hi*hi + hi*lo + lo*hi, each exact in FP32.
+template <int M, int TAPS, int F16>
 __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
+  constexpr int kKC = tc_kc(F16);  // frames per pipeline stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const SegDev sd = a.segs[blockIdx.y];
   if (!sd.wpe_active) return;
@@ -137,16 +165,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   const int SF = kKC + H + kLook;  // slab frames per chunk
 
   // shared memory carve-up
-  const int NS = tc_stages(km, M, H);                                    // operand buffers / accumulator sets
+  const int NS = tc_stages(km, M, H, kKC);                               // operand buffers / accumulator sets
   const uint32_t setw = NS == 3 ? 160u : 256u;                        // tensor-memory columns per accumulator set
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);             // [3] operands of a chunk are staged
   uint64_t* done = full + 3;                                          // [3] MMAs of a chunk are complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + 64);
-  float* wbuf = reinterpret_cast<float*>(smem_raw + 128);             // [3][kKC] Gram weights
+  float* red = reinterpret_cast<float*>(smem_raw + 128);              // [2 parities][slab, weight][16 warps] stage maxima (F16)
+  float* wbuf = reinterpret_cast<float*>(smem_raw + kHead);           // [3][kKC] Gram weights
   float* planes = wbuf + 3 * kKC;                                     // [3 stages][re, im][SF * M]
   const int plane_words = SF * M;
-  const size_t off = tc_head_bytes(M, H);
-  const int buf_words = NB * kKC;                                     // one operand buffer (hi or lo)
+  const size_t off = tc_head_bytes(M, H, kKC);
+  const int buf_words = NB * kKW;                                     // one operand buffer (hi or lo)
   float* opbuf = reinterpret_cast<float*>(smem_raw + off);            // [stage][hi/lo][buf_words]
 
   if (tid == 0) {
@@ -175,7 +204,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   if (warp == kTcWorkerWarps) {
     // ===== MMA issuer =====
     if (lane == 0) {
-      const uint32_t idesc1 = make_idesc_tf32(NR), idesc2 = make_idesc_tf32(N2 > 0 ? N2 : 16, 64);
+      const uint32_t idesc1 = F16 ? make_idesc_f16(NR) : make_idesc_tf32(NR);
+      const uint32_t idesc2 = F16 ? make_idesc_f16(N2 > 0 ? N2 : 16, 64) : make_idesc_tf32(N2 > 0 ? N2 : 16, 64);
+      auto mma = [](uint32_t d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+        if constexpr (F16) mma_f16(d, da, db, idesc, acc);
+        else mma_tf32(d, da, db, idesc, acc);
+      };
       // The corner (rows and columns >= 128) is read back only where an Im a row lies beyond row 127, i.e. when
       // KMP + km > 128 (M = 7, 8). At M = 6 rows 128.. are the y rows, needed as columns only: no corner MMAs, and
       // since every MMA costs ~150 cycles whatever its shape (tools/mma_probe.cu) that is half of the MMA stream.
@@ -187,13 +221,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
         const uint32_t a_hi = smem_u32(opbuf + (size_t)(2 * b) * buf_words), a_lo = a_hi + 4u * (uint32_t)buf_words;
         const uint32_t d1 = tmem_base + (uint32_t)b * setw, d2 = d1 + (uint32_t)NR;
 #pragma unroll
-        for (int ks = 0; ks < kKC / 8; ++ks) {
+        for (int ks = 0; ks < kKW / 8; ++ks) {  // 32 bytes of K per MMA: 8 TF32 or 16 FP16 frames
           const uint32_t accf = ks > 0 ? 1u : 0u;  // every chunk starts its accumulator set from zero
           const uint32_t ko = ks * 256;            // two core matrices along K per MMA
           const uint64_t dh = make_smem_desc(a_hi + ko, lbo, sbo), dl = make_smem_desc(a_lo + ko, lbo, sbo);
-          mma_tf32(d1, dh, dh, idesc1, accf);
-          mma_tf32(d1, dh, dl, idesc1, 1u);
-          mma_tf32(d1, dl, dh, idesc1, 1u);
+          mma(d1, dh, dh, idesc1, accf);
+          mma(d1, dh, dl, idesc1, 1u);
+          mma(d1, dl, dh, idesc1, 1u);
           if (corner) {
             // the corner is an M = 64 MMA on the last 64 rows: the kernel is bound by the operand bytes it
             // streams from shared memory, and a 64-row A tile is half of them (row r of that accumulator
@@ -201,9 +235,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
             const uint32_t ra = ((NR - 64) / 8) * sbo, rb = 16 * sbo;  // rows NR-64.. and rows 128..
             const uint64_t ah = make_smem_desc(a_hi + ra + ko, lbo, sbo), al = make_smem_desc(a_lo + ra + ko, lbo, sbo);
             const uint64_t bh = make_smem_desc(a_hi + rb + ko, lbo, sbo), bl = make_smem_desc(a_lo + rb + ko, lbo, sbo);
-            mma_tf32(d2, ah, bh, idesc2, accf);
-            mma_tf32(d2, ah, bl, idesc2, 1u);
-            mma_tf32(d2, al, bh, idesc2, 1u);
+            mma(d2, ah, bh, idesc2, accf);
+            mma(d2, ah, bl, idesc2, 1u);
+            mma(d2, al, bh, idesc2, 1u);
           }
         }
         tc_commit(&done[b]);
@@ -250,7 +284,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     for (int i = 0; i < kAccPerThread; ++i) acc[i] = 0.f;
     const int q = warp & 3, qcol = (warp >> 2) * NCQ;
 
+    // F16: 2^(-2 e) of the stage whose accumulators sit in set 0 / 1 / 2 (a power of two: the rescale is exact)
+    float inv2_0 = 1.f, inv2_1 = 1.f, inv2_2 = 1.f;
     auto drain = [&](int set) {
+      const float inv2 = set == 0 ? inv2_0 : set == 1 ? inv2_1 : inv2_2;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)set * setw + (uint32_t)qcol;
       constexpr int kBatch = 32;  // columns in flight per wait
 #pragma unroll
@@ -272,7 +309,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
           const int col = b0 + j * 8;
           if (col < kAccPerThread && col < NCQ) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[col + i] += __uint_as_float(v[j * 8 + i]);
+            for (int i = 0; i < 8; ++i) {
+              if constexpr (F16) acc[col + i] = fmaf(__uint_as_float(v[j * 8 + i]), inv2, acc[col + i]);
+              else acc[col + i] += __uint_as_float(v[j * 8 + i]);
+            }
           }
         }
       }
@@ -281,14 +321,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     // expand: warp w owns k chunk w (frames 4w .. 4w+3) and walks all row groups; lane -> (row rg*8 + lane/4,
     // frame 4w + lane%4), so a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
     static_assert(kTcWorkerWarps == kKCores, "one worker warp per K chunk");
-    const int k = warp * 4 + (lane & 3), r8 = lane >> 2;
+    // FP32 words hold one frame, FP16 words a pair: lane % 4 picks frame k (TF32) or frames k, k + 1 (FP16) of the
+    // warp's core matrix
+    const int k = F16 ? warp * 8 + 2 * (lane & 3) : warp * 4 + (lane & 3), r8 = lane >> 2;
     const int word0 = warp * kCoreWords + lane;  // core (rg, kc = warp) -> (rg * kKCores + warp) * 32 + lane
     // row groups that carry data: [Re a | Im a | Re y | Im y]; the groups after them (padding up to NB rows: a third
     // of the 128-row tile at M = 4) are zero in every chunk, so they are zeroed once here and never rewritten
     const int nrg_a = KMP / 8, nrg = 2 * nrg_a + 2;
-    for (int i = tid; i < 2 * NS * (NB - 8 * nrg) * kKC; i += kTcWorkers) {
-      const int per = (NB - 8 * nrg) * kKC;  // zero words per operand buffer
-      opbuf[(size_t)(i / per) * buf_words + (size_t)(8 * nrg) * kKC + (i % per)] = 0.f;
+    for (int i = tid; i < 2 * NS * (NB - 8 * nrg) * kKW; i += kTcWorkers) {
+      const int per = (NB - 8 * nrg) * kKW;  // zero words per operand buffer
+      opbuf[(size_t)(i / per) * buf_words + (size_t)(8 * nrg) * kKW + (i % per)] = 0.f;
     }
 
     issue_slab(0);
@@ -312,23 +354,76 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
       const float* im = re + plane_words;
       float* hi_buf = opbuf + (size_t)(2 * b) * buf_words;
       float* lo_buf = hi_buf + buf_words;
-      const float sq = sqrt_approx_tc(wbuf[st * kKC + k]);
       const float* rk = re + k * M + r8;
       const float* ik = im + k * M + r8;
+      if constexpr (F16) {
+        // stage scale: a bound of |x| sqrt(w) over the stage = (largest slab magnitude) x (largest sqrt(w))
+        float mx = 0.f, mw = 0.f;
+        for (int i = tid; i < plane_words; i += kTcWorkers) mx = fmaxf(mx, fmaxf(fabsf(re[i]), fabsf(im[i])));
+        if (tid < kKC) mw = wbuf[st * kKC + tid];
 #pragma unroll
-      for (int rg = 0; rg < 24; ++rg) {  // NB <= 192 rows
-        if (rg < nrg) {
-          // (loading every row group's value ahead of the stores was measured: 8.74 against 8.32 ms at M = 4)
-          float v;
-          if (rg < nrg_a) v = rk[rg * 8];                              // Re a: element rg*8 + r8 of the window
-          else if (rg < 2 * nrg_a) v = ik[(rg - nrg_a) * 8];           // Im a
-          else if (rg == 2 * nrg_a) v = rk[H * M];                     // Re y (rows >= M are never read back)
-          else if (rg == 2 * nrg_a + 1) v = ik[H * M];                 // Im y
-          else v = 0.f;
-          v *= sq;
-          const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-          hi_buf[rg * (kKCores * kCoreWords) + word0] = hi;
-          lo_buf[rg * (kKCores * kCoreWords) + word0] = v - hi;
+        for (int o = 16; o > 0; o >>= 1) {
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+        }
+        float* rd = red + (c & 1) * 32;  // [16 warps] slab maxima, [16 warps] weight maxima
+        if (lane == 0) {
+          rd[warp] = mx;
+          rd[16 + warp] = mw;
+        }
+        workers_sync();
+        mx = fmaxf(rd[lane & 15], 0.f);
+        mw = rd[16 + (lane & 15)];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+        }
+        const float bound = mx * sqrt_approx_tc(mw) * 1.0001f;  // sqrt.approx is within 2 ulp
+        // bound < 2^(eb + 1): scale by 2^(14 - eb). The exponent is clamped so that 2^(-2 e) stays a normal float;
+        // a zero, infinite or NaN bound lands on a clamp and the values go through as they are (0, Inf, NaN).
+        const int eb = (int)((__float_as_uint(bound) >> 23) & 255u) - 127;
+        const int es = min(60, max(-60, 14 - eb));
+        const float scl = __uint_as_float((uint32_t)(es + 127) << 23);
+        const float inv2 = __uint_as_float((uint32_t)(127 - 2 * es) << 23);
+        if (b == 0) inv2_0 = inv2;
+        else if (b == 1) inv2_1 = inv2;
+        else inv2_2 = inv2;
+        const float sq0 = sqrt_approx_tc(wbuf[st * kKC + k]) * scl, sq1 = sqrt_approx_tc(wbuf[st * kKC + k + 1]) * scl;
+#pragma unroll
+        for (int rg = 0; rg < 24; ++rg) {  // NB <= 192 rows
+          if (rg < nrg) {
+            float v0, v1;
+            if (rg < nrg_a) v0 = rk[rg * 8], v1 = rk[rg * 8 + M];                              // Re a
+            else if (rg < 2 * nrg_a) v0 = ik[(rg - nrg_a) * 8], v1 = ik[(rg - nrg_a) * 8 + M];  // Im a
+            else if (rg == 2 * nrg_a) v0 = rk[H * M], v1 = rk[H * M + M];                      // Re y
+            else v0 = ik[H * M], v1 = ik[H * M + M];                                           // Im y
+            v0 *= sq0;
+            v1 *= sq1;
+            const __half2 hi = __floats2half2_rn(v0, v1);
+            const float2 hf = __half22float2(hi);
+            const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+            reinterpret_cast<__half2*>(hi_buf)[rg * (kKCores * kCoreWords) + word0] = hi;
+            reinterpret_cast<__half2*>(lo_buf)[rg * (kKCores * kCoreWords) + word0] = lo;
+          }
+        }
+      } else {
+        const float sq = sqrt_approx_tc(wbuf[st * kKC + k]);
+#pragma unroll
+        for (int rg = 0; rg < 24; ++rg) {  // NB <= 192 rows
+          if (rg < nrg) {
+            // (loading every row group's value ahead of the stores was measured: 8.74 against 8.32 ms at M = 4)
+            float v;
+            if (rg < nrg_a) v = rk[rg * 8];                              // Re a: element rg*8 + r8 of the window
+            else if (rg < 2 * nrg_a) v = ik[(rg - nrg_a) * 8];           // Im a
+            else if (rg == 2 * nrg_a) v = rk[H * M];                     // Re y (rows >= M are never read back)
+            else if (rg == 2 * nrg_a + 1) v = ik[H * M];                 // Im y
+            else v = 0.f;
+            v *= sq;
+            const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+            hi_buf[rg * (kKCores * kCoreWords) + word0] = hi;
+            lo_buf[rg * (kKCores * kCoreWords) + word0] = v - hi;
+          }
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core reads
@@ -364,23 +459,27 @@ int wpe_tc_supported(int km, int M) {
 int wpe_tc_cell_floats(int km, int M) { return 128 * tc_cols(km, M); }
 int wpe_tc_rows(int km, int M) { return tc_rows(km, M); }
 
+template <int M, int TAPS, int F16>
+static cudaError_t launch_tc_k(const WpeArgs& a, int nseg, int F, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(wpe_gram_tc_kernel<M, TAPS, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  wpe_gram_tc_kernel<M, TAPS, F16><<<dim3(F, nseg), kTcThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <int M>
 static cudaError_t launch_tc_m(const WpeArgs& a, int nseg, int F, cudaStream_t st) {
   const int km = a.taps * M, H = a.delay + a.taps - 1;
-  size_t smem = tc_smem_bytes(km, M, H, tc_stages(km, M, H));
+  // the FP16 kind stages twice the frames: a long history that no longer fits runs the TF32 kind
+  int f16 = a.gram_f16;
+  if (f16 && tc_smem_bytes(km, M, H, 2, tc_kc(1)) > 224 * 1024) f16 = 0;
+  const int kc = tc_kc(f16);
+  size_t smem = tc_smem_bytes(km, M, H, tc_stages(km, M, H, kc), kc);
   if (smem > 224 * 1024) return cudaErrorInvalidConfiguration;
   // all 512 tensor-memory columns belong to one CTA: keep a second CTA off the SM
   smem = std::max<size_t>(smem, 120 * 1024);
-  if (a.taps == 10) {
-    cudaError_t e = cudaFuncSetAttribute(wpe_gram_tc_kernel<M, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    wpe_gram_tc_kernel<M, 10><<<dim3(F, nseg), kTcThreads, smem, st>>>(a);
-  } else {
-    cudaError_t e = cudaFuncSetAttribute(wpe_gram_tc_kernel<M, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    wpe_gram_tc_kernel<M, 0><<<dim3(F, nseg), kTcThreads, smem, st>>>(a);
-  }
-  return cudaGetLastError();
+  if (a.taps == 10) return f16 ? launch_tc_k<M, 10, 1>(a, nseg, F, smem, st) : launch_tc_k<M, 10, 0>(a, nseg, F, smem, st);
+  return f16 ? launch_tc_k<M, 0, 1>(a, nseg, F, smem, st) : launch_tc_k<M, 0, 0>(a, nseg, F, smem, st);
 }
 
 cudaError_t launch_wpe_gram_tc(const WpeArgs& a, int nseg, int F, cudaStream_t st) {
