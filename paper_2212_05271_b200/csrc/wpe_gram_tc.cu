@@ -36,7 +36,7 @@ constexpr int kKCores = kKW / 4;            // core matrices along K per row gro
 // (8 per warp): an MMA costs ~150 cycles whatever its shape or kind (tools/mma_probe.cu), so the FP16 split halves
 // the MMA stream per frame -- and the operand bytes, drains and barriers with it.
 __host__ __device__ constexpr int tc_kc(int f16) { return f16 ? 128 : 64; }
-constexpr int kHead = 384;                  // barriers, the tensor-memory slot, the scale reduction scratch
+constexpr int kHead = 256;                  // barriers, the tensor-memory slot, the scale reduction scratch
 constexpr int kLook = 8;                    // look-ahead frames read by the padded rows
 constexpr int kAccPerThread = 56;           // register accumulators per thread: NCT <= 224 columns / 4 quarters
 
@@ -49,7 +49,8 @@ __host__ __device__ inline int tc_n2(int km, int M) { return tc_rows(km, M) > 12
 __host__ __device__ inline int tc_cols(int km, int M) { return tc_rows(km, M) + tc_n2(km, M); }         // D1 | D2
 /// Bytes ahead of the operand buffers: barriers, Gram weights, three stages of planar slabs (H = history frames).
 __host__ __device__ inline size_t tc_head_bytes(int M, int H, int kc) {
-  const size_t off = kHead + sizeof(float) * (3 * kc + 6 * (size_t)(kc + H + kLook) * M);
+  // Gram weights [3][kc], slab planes [3][re, im][frames * M], per-frame slab maxima [frames] (FP16 kind)
+  const size_t off = kHead + sizeof(float) * (3 * kc + (6 * (size_t)M + 1) * (size_t)(kc + H + kLook));
   return (off + 127) & ~(size_t)127;
 }
 __host__ __device__ inline size_t tc_smem_bytes(int km, int M, int H, int stages, int kc) {
@@ -170,10 +171,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);             // [3] operands of a chunk are staged
   uint64_t* done = full + 3;                                          // [3] MMAs of a chunk are complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + 64);
-  float* red = reinterpret_cast<float*>(smem_raw + 128);              // [2 parities][slab, weight][16 warps] stage maxima (F16)
+  float* red = reinterpret_cast<float*>(smem_raw + 128);              // [2 parities][history, current frame][4 warps] stage maxima (F16)
   float* wbuf = reinterpret_cast<float*>(smem_raw + kHead);           // [3][kKC] Gram weights
   float* planes = wbuf + 3 * kKC;                                     // [3 stages][re, im][SF * M]
   const int plane_words = SF * M;
+  float* fmx = planes + 6 * plane_words;                              // [SF] largest |re|, |im| of a slab frame (F16)
   const size_t off = tc_head_bytes(M, H, kKC);
   const int buf_words = NB * kKW;                                     // one operand buffer (hi or lo)
   float* opbuf = reinterpret_cast<float*>(smem_raw + off);            // [stage][hi/lo][buf_words]
@@ -284,10 +286,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     for (int i = 0; i < kAccPerThread; ++i) acc[i] = 0.f;
     const int q = warp & 3, qcol = (warp >> 2) * NCQ;
 
-    // F16: 2^(-2 e) of the stage whose accumulators sit in set 0 / 1 / 2 (a power of two: the rescale is exact)
-    float inv2_0 = 1.f, inv2_1 = 1.f, inv2_2 = 1.f;
+    // F16: the rescale factors of the stage whose accumulators sit in set 0 / 1 / 2: 2^-(ea + ea) for a product of two
+    // history rows, 2^-(ea + ey) for history x current frame (powers of two: the rescale is exact)
+    float iaa_0 = 1.f, iaa_1 = 1.f, iaa_2 = 1.f, iay_0 = 1.f, iay_1 = 1.f, iay_2 = 1.f;
     auto drain = [&](int set) {
-      const float inv2 = set == 0 ? inv2_0 : set == 1 ? inv2_1 : inv2_2;
+      const float iaa = set == 0 ? iaa_0 : set == 1 ? iaa_1 : iaa_2;
+      const float iay = set == 0 ? iay_0 : set == 1 ? iay_1 : iay_2;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)set * setw + (uint32_t)qcol;
       constexpr int kBatch = 32;  // columns in flight per wait
 #pragma unroll
@@ -308,9 +312,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
         for (int j = 0; j < kBatch / 8; ++j) {
           const int col = b0 + j * 8;
           if (col < kAccPerThread && col < NCQ) {
+            // columns of D1 are operand rows 0..NR-1, those of D2 rows 128..NR-1; rows >= 2 KMP are the current frame
+            const int gc = qcol + col, orow = gc < NR ? gc : 128 + (gc - NR);
+            const float inv = orow >= 2 * KMP ? iay : iaa;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              if constexpr (F16) acc[col + i] = fmaf(__uint_as_float(v[j * 8 + i]), inv2, acc[col + i]);
+              if constexpr (F16) acc[col + i] = fmaf(__uint_as_float(v[j * 8 + i]), inv, acc[col + i]);
               else acc[col + i] += __uint_as_float(v[j * 8 + i]);
             }
           }
@@ -357,39 +364,54 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
       const float* rk = re + k * M + r8;
       const float* ik = im + k * M + r8;
       if constexpr (F16) {
-        // stage scale: a bound of |x| sqrt(w) over the stage = (largest slab magnitude) x (largest sqrt(w))
-        float mx = 0.f, mw = 0.f;
-        for (int i = tid; i < plane_words; i += kTcWorkers) mx = fmaxf(mx, fmaxf(fabsf(re[i]), fabsf(im[i])));
-        if (tid < kKC) mw = wbuf[st * kKC + tid];
+        // Stage scales: the exact largest |x| sqrt(w) over the history rows and over the current-frame rows of the
+        // stage. Two, because the two differ by the signal's short-term dynamic range (a burst in the history of a
+        // near-silent frame is 10^7 times that frame's own normalised value) and every product needs its smaller
+        // factor at full precision too: P = sum w a y^H. An element e of the window of stage frame k is slab word
+        // k M + e, i.e. slab frames k .. k + taps (the padded rows reach one frame further); the current frame is k + H.
+        for (int fr = tid; fr < SF; fr += kTcWorkers) {
+          float m = 0.f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
-        }
-        float* rd = red + (c & 1) * 32;  // [16 warps] slab maxima, [16 warps] weight maxima
-        if (lane == 0) {
-          rd[warp] = mx;
-          rd[16 + warp] = mw;
+          for (int ch = 0; ch < M; ++ch) m = fmaxf(m, fmaxf(fabsf(re[fr * M + ch]), fabsf(im[fr * M + ch])));
+          fmx[fr] = m;
         }
         workers_sync();
-        mx = fmaxf(rd[lane & 15], 0.f);
-        mw = rd[16 + (lane & 15)];
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+        float ma = 0.f, my = 0.f;
+        if (tid < kKC) {
+          const float sqk = sqrt_approx_tc(wbuf[st * kKC + tid]);
+          for (int u = 0; u <= taps; ++u) ma = fmaxf(ma, fmx[tid + u]);
+          my = fmaxf(fmx[tid + H], fmx[tid + H + 1]) * sqk;
+          ma *= sqk;
         }
-        const float bound = mx * sqrt_approx_tc(mw) * 1.0001f;  // sqrt.approx is within 2 ulp
-        // bound < 2^(eb + 1): scale by 2^(14 - eb). The exponent is clamped so that 2^(-2 e) stays a normal float;
-        // a zero, infinite or NaN bound lands on a clamp and the values go through as they are (0, Inf, NaN).
-        const int eb = (int)((__float_as_uint(bound) >> 23) & 255u) - 127;
-        const int es = min(60, max(-60, 14 - eb));
-        const float scl = __uint_as_float((uint32_t)(es + 127) << 23);
-        const float inv2 = __uint_as_float((uint32_t)(127 - 2 * es) << 23);
-        if (b == 0) inv2_0 = inv2;
-        else if (b == 1) inv2_1 = inv2;
-        else inv2_2 = inv2;
-        const float sq0 = sqrt_approx_tc(wbuf[st * kKC + k]) * scl, sq1 = sqrt_approx_tc(wbuf[st * kKC + k + 1]) * scl;
+        float* rd = red + (c & 1) * 8;  // [4 warps] history maxima, [4 warps] current-frame maxima
+        if (warp < kKC / 32) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+            my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
+          }
+          if (lane == 0) {
+            rd[warp] = ma;
+            rd[4 + warp] = my;
+          }
+        }
+        workers_sync();
+        ma = fmaxf(fmaxf(rd[0], rd[1]), fmaxf(rd[2], rd[3]));
+        my = fmaxf(fmaxf(rd[4], rd[5]), fmaxf(rd[6], rd[7]));
+        // bound < 2^(eb + 1): scale by 2^(14 - eb). The exponents are clamped so that the rescale factors stay
+        // normal floats; a zero, infinite or NaN bound lands on a clamp and the values go through as they are.
+        auto scale_exp = [](float bound) {
+          const int eb = (int)((__float_as_uint(bound) >> 23) & 255u) - 127;
+          return min(60, max(-60, 14 - eb));
+        };
+        const int ea = scale_exp(ma), ey = scale_exp(my);
+        const float scl_a = __uint_as_float((uint32_t)(ea + 127) << 23), scl_y = __uint_as_float((uint32_t)(ey + 127) << 23);
+        const float iaa = __uint_as_float((uint32_t)(127 - 2 * ea) << 23), iay = __uint_as_float((uint32_t)(127 - ea - ey) << 23);
+        if (b == 0) iaa_0 = iaa, iay_0 = iay;
+        else if (b == 1) iaa_1 = iaa, iay_1 = iay;
+        else iaa_2 = iaa, iay_2 = iay;
+        const float sqk0 = sqrt_approx_tc(wbuf[st * kKC + k]), sqk1 = sqrt_approx_tc(wbuf[st * kKC + k + 1]);
+        const float sa0 = sqk0 * scl_a, sa1 = sqk1 * scl_a, sy0 = sqk0 * scl_y, sy1 = sqk1 * scl_y;
 #pragma unroll
         for (int rg = 0; rg < 24; ++rg) {  // NB <= 192 rows
           if (rg < nrg) {
@@ -398,8 +420,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
             else if (rg < 2 * nrg_a) v0 = ik[(rg - nrg_a) * 8], v1 = ik[(rg - nrg_a) * 8 + M];  // Im a
             else if (rg == 2 * nrg_a) v0 = rk[H * M], v1 = rk[H * M + M];                      // Re y
             else v0 = ik[H * M], v1 = ik[H * M + M];                                           // Im y
-            v0 *= sq0;
-            v1 *= sq1;
+            v0 *= rg < 2 * nrg_a ? sa0 : sy0;
+            v1 *= rg < 2 * nrg_a ? sa1 : sy1;
             const __half2 hi = __floats2half2_rn(v0, v1);
             const float2 hf = __half22float2(hi);
             const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);

@@ -200,6 +200,75 @@ def test_wpe_tensor_core_kernels_match_the_fp32_kernels_at_full_width(gss):
     assert np.abs(got - want).max() < 1e-3 * np.abs(want).max()
 
 
+def _gram_float64(y, taps, delay, floor=1e-10):
+    """R = sum_t w_t a_t a_t^H and P = sum_t w_t a_t y_t^H in float64, weights as the device forms them (wpe.hpp:40-89)."""
+    f, t, m = y.shape
+    km, h = taps * m, delay + taps - 1
+    R = np.zeros((f, km, km), np.complex128)
+    P = np.zeros((f, km, m), np.complex128)
+    for ff in range(f):
+        yf = y[ff].astype(np.complex128)
+        pw = (np.abs(y[ff]) ** 2).astype(np.float32).sum(1)
+        lam = np.maximum(np.float32(floor), (pw.astype(np.float64) / m).astype(np.float32))
+        w = (np.float32(1.0) / lam).astype(np.float64)
+        pad = np.vstack([np.zeros((h, m), np.complex128), yf])
+        A = np.stack([pad[tt: tt + taps].reshape(-1) for tt in range(t)])
+        R[ff] = (A.T * w) @ A.conj()
+        P[ff] = (A.T * w) @ yf.conj()
+    return R, P
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["f16", "tf32"])
+@pytest.mark.parametrize("m, t", [(8, 700), (4, 333), (5, 1000)])
+def test_wpe_tensor_core_gram_over_a_wide_dynamic_range(gss, kind, m, t):
+    # The FP16 kind scales every 128-frame stage by a power of two; loud bursts next to near-silence, exact zeros
+    # and very small / very large overall levels are where a fixed-range format would lose the Gram. Both kinds must
+    # stay at FP32-sum accuracy against a float64 evaluation.
+    import ctypes as C
+    import os
+    from paper_2212_05271_b200 import capi
+    rng = np.random.RandomState(m * 1000 + t)
+    f, taps, delay = 3, 10, 2
+    y = (rng.randn(f, t, m) + 1j * rng.randn(f, t, m)).astype(np.complex64)
+    y[:, 3:] += 0.6 * y[:, :-3]
+    env = np.ones(t, np.float32)
+    env[40:60] = 1e3        # a burst
+    env[60:200] = 1e-4      # near-silence right after it (its history holds the burst)
+    env[260:300] = 0.0      # digital silence: the power floor is the weight
+    env[300:] *= np.exp(rng.randn(t - 300)).astype(np.float32)
+    y *= env[None, :, None]
+    y[0] *= 1e-6            # overall level per bin
+    y[2] *= 1e4
+    old = os.environ.get("GSS_B200_WPE_GRAM_KIND")
+    os.environ["GSS_B200_WPE_GRAM_KIND"] = kind
+    os.environ["GSS_B200_WPE_GRAM"] = "tc"
+    try:
+        ctx = gss.Context(0)  # the switches are read when a context is created
+        cfg = capi.WpeConfig(taps, delay, 1, 0, 1e-10)
+        km = taps * m
+        out = np.zeros((f, km * km + km * m), np.complex128)
+        ctx.check(ctx.lib.gss_b200_debug_wpe_gram(ctx.handle, capi.ptr(y), C.c_int32(f), C.c_int64(t), C.c_int32(m),
+                                                  C.byref(cfg), capi.ptr(out)))
+        ctx.close()
+    finally:
+        os.environ.pop("GSS_B200_WPE_GRAM", None)
+        if old is None:
+            os.environ.pop("GSS_B200_WPE_GRAM_KIND", None)
+        else:
+            os.environ["GSS_B200_WPE_GRAM_KIND"] = old
+    R = out[:, : km * km].reshape(f, km, km)
+    P = out[:, km * km:].reshape(f, km, m)
+    Rr, Pr = _gram_float64(y, taps, delay)
+    for ff in range(f):
+        # the regularisation the solve adds is not part of the dumped Gram; compare bin by bin (levels differ by 1e10)
+        assert rel_fro(R[ff], Rr[ff]) < 3e-6, (kind, ff, rel_fro(R[ff], Rr[ff]))
+        assert rel_fro(P[ff], Pr[ff]) < 3e-6, (kind, ff, rel_fro(P[ff], Pr[ff]))
+        # entry-wise against the diagonal scale: no row or column loses its small entries
+        d = np.sqrt(np.abs(np.diag(Rr[ff])).clip(1e-300))
+        assert (np.abs(R[ff] - Rr[ff]) / np.outer(d, d)).max() < 1e-5, (kind, ff)
+
+
 def test_wpe_eigen_floor_fallback_many_bins_at_once(gss, oracle):
     # every one of 48 bins (more than the 32 scratch slots of a launch) needs the fallback with a 40 x 40
     # system: the blocks queue for slots instead of failing, and the block-parallel Jacobi keeps it quick
