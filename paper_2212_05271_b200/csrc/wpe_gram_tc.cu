@@ -328,9 +328,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
     // expand: warp w owns k chunk w (frames 4w .. 4w+3) and walks all row groups; lane -> (row rg*8 + lane/4,
     // frame 4w + lane%4), so a warp store is one 8 x 16-byte core matrix = 128 contiguous bytes
     static_assert(kTcWorkerWarps == kKCores, "one worker warp per K chunk");
-    // FP32 words hold one frame, FP16 words a pair: lane % 4 picks frame k (TF32) or frames k, k + 1 (FP16) of the
-    // warp's core matrix
-    const int k = F16 ? warp * 8 + 2 * (lane & 3) : warp * 4 + (lane & 3), r8 = lane >> 2;
+    // FP32 words hold one frame, FP16 words a pair: lane % 4 picks frame k (TF32) or frames k, k + 4 (FP16) of the
+    // warp's core matrix. (Which frame sits in which K slot is free -- both MMA operands are this one buffer -- and
+    // with the pair 4 apart the 32 lanes read 32 different banks of the slab, and, M even, share most of their loads.)
+    const int k = F16 ? warp * 8 + (lane & 3) : warp * 4 + (lane & 3), r8 = lane >> 2;
     const int word0 = warp * kCoreWords + lane;  // core (rg, kc = warp) -> (rg * kKCores + warp) * 32 + lane
     // row groups that carry data: [Re a | Im a | Re y | Im y]; the groups after them (padding up to NB rows: a third
     // of the 128-row tile at M = 4) are zero in every chunk, so they are zeroed once here and never rewritten
@@ -410,25 +411,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) wpe_gram_tc_kernel(WpeArgs a) {
         if (b == 0) iaa_0 = iaa, iay_0 = iay;
         else if (b == 1) iaa_1 = iaa, iay_1 = iay;
         else iaa_2 = iaa, iay_2 = iay;
-        const float sqk0 = sqrt_approx_tc(wbuf[st * kKC + k]), sqk1 = sqrt_approx_tc(wbuf[st * kKC + k + 1]);
+        const float sqk0 = sqrt_approx_tc(wbuf[st * kKC + k]), sqk1 = sqrt_approx_tc(wbuf[st * kKC + k + 4]);
         const float sa0 = sqk0 * scl_a, sa1 = sqk1 * scl_a, sy0 = sqk0 * scl_y, sy1 = sqk1 * scl_y;
+        auto put = [&](int rg, float v0, float v1) {
+          const __half2 hi = __floats2half2_rn(v0, v1);
+          const float2 hf = __half22float2(hi);
+          const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+          reinterpret_cast<__half2*>(hi_buf)[rg * (kKCores * kCoreWords) + word0] = hi;
+          reinterpret_cast<__half2*>(lo_buf)[rg * (kKCores * kCoreWords) + word0] = lo;
+        };
+        if constexpr (M % 2 == 0) {
+          // Window element e of frame k + 4 is element e + 4 M of frame k: row group rg of the later frame is row
+          // group rg + M / 2 of the earlier one. One run of loads (issued together, ahead of the stores the compiler
+          // cannot move them across) serves both frames.
+          constexpr int SH = M / 2, NX = 10 + SH;  // km <= 80: at most 10 row groups per part
+          auto part = [&](const float* src, int rg0) {
+            float x[NX];
 #pragma unroll
-        for (int rg = 0; rg < 24; ++rg) {  // NB <= 192 rows
-          if (rg < nrg) {
-            float v0, v1;
-            if (rg < nrg_a) v0 = rk[rg * 8], v1 = rk[rg * 8 + M];                              // Re a
-            else if (rg < 2 * nrg_a) v0 = ik[(rg - nrg_a) * 8], v1 = ik[(rg - nrg_a) * 8 + M];  // Im a
-            else if (rg == 2 * nrg_a) v0 = rk[H * M], v1 = rk[H * M + M];                      // Re y
-            else v0 = ik[H * M], v1 = ik[H * M + M];                                           // Im y
-            v0 *= rg < 2 * nrg_a ? sa0 : sy0;
-            v1 *= rg < 2 * nrg_a ? sa1 : sy1;
-            const __half2 hi = __floats2half2_rn(v0, v1);
-            const float2 hf = __half22float2(hi);
-            const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
-            reinterpret_cast<__half2*>(hi_buf)[rg * (kKCores * kCoreWords) + word0] = hi;
-            reinterpret_cast<__half2*>(lo_buf)[rg * (kKCores * kCoreWords) + word0] = lo;
+            for (int i = 0; i < NX; ++i) x[i] = i < nrg_a + SH ? src[i * 8] : 0.f;
+#pragma unroll
+            for (int rg = 0; rg < 10; ++rg)
+              if (rg < nrg_a) put(rg0 + rg, x[rg] * sa0, x[rg + SH] * sa1);
+          };
+          part(rk, 0);       // Re a
+          part(ik, nrg_a);   // Im a
+        } else {
+#pragma unroll
+          for (int rg = 0; rg < 20; ++rg) {
+            if (rg < 2 * nrg_a) {
+              const float* src = rg < nrg_a ? rk + rg * 8 : ik + (rg - nrg_a) * 8;
+              put(rg, src[0] * sa0, src[4 * M] * sa1);
+            }
           }
         }
+        put(2 * nrg_a, rk[H * M] * sy0, rk[H * M + 4 * M] * sy1);      // Re y (rows >= M are never read back)
+        put(2 * nrg_a + 1, ik[H * M] * sy0, ik[H * M + 4 * M] * sy1);  // Im y
       } else {
         const float sq = sqrt_approx_tc(wbuf[st * kKC + k]);
 #pragma unroll
