@@ -80,6 +80,7 @@ struct gss_b200_ctx {
   int wpe_gram_tc = 2;
   int wpe_gram_f16 = 1;      // tensor-core Gram operand split: 1 = FP16 (K = 16 per MMA), 0 = TF32 (GSS_B200_WPE_GRAM_KIND = tf32)
   int wpe_apply_tc = 2;
+  int wpe_apply_f16 = 1;     // tensor-core prediction operand split, as wpe_gram_f16 (GSS_B200_WPE_APPLY_KIND = tf32)
   int em_chunk_frames = 0;   // debug knob: force the EM frame chunk (0 = automatic)
   int wpe_chunk_frames = 0;  // debug knob: force the WPE frame chunk (0 = one chunk)
   // Shape groups of one batch (segments sharing channel count and class tier) are independent: they are enqueued
@@ -567,6 +568,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
   a.gram_f16 = c->wpe_gram_f16;
+  a.apply_f16 = c->wpe_apply_f16;
   a.apply_tc = (c->wpe_apply_tc == 1 || (c->wpe_apply_tc == 2 && g.M >= 5)) &&
                wpe_apply_tc_supported(w.taps, w.delay, g.M);
   a.debug_rp = nullptr;
@@ -819,6 +821,7 @@ gss_status gss_b200_create(int device, gss_b200_ctx** out) {
   }
   if (const char* s = std::getenv("GSS_B200_WPE_GRAM")) c->wpe_gram_tc = std::strcmp(s, "fp32") == 0 ? 0 : std::strcmp(s, "tc") == 0 ? 1 : 2;
   if (const char* s = std::getenv("GSS_B200_WPE_GRAM_KIND")) c->wpe_gram_f16 = std::strcmp(s, "tf32") == 0 ? 0 : 1;
+  if (const char* s = std::getenv("GSS_B200_WPE_APPLY_KIND")) c->wpe_apply_f16 = std::strcmp(s, "tf32") == 0 ? 0 : 1;
   if (const char* s = std::getenv("GSS_B200_WPE_APPLY")) c->wpe_apply_tc = std::strcmp(s, "fp32") == 0 ? 0 : std::strcmp(s, "tc") == 0 ? 1 : 2;
   if (const char* s = std::getenv("GSS_B200_EM_CHUNK_FRAMES")) c->em_chunk_frames = std::atoi(s);
   if (const char* s = std::getenv("GSS_B200_WPE_CHUNK_FRAMES")) c->wpe_chunk_frames = std::atoi(s);
@@ -1588,6 +1591,7 @@ gss_status gss_b200_debug_wpe_gram(gss_b200_ctx* c, const float* in, int32_t bin
   a.gram_raw = g.gram_raw;
   a.use_tc = g.use_tc;
   a.gram_f16 = c->wpe_gram_f16;
+  a.apply_f16 = c->wpe_apply_f16;
   a.apply_tc = 0;
   a.w_next = nullptr;
   a.debug_rp = d_rp;

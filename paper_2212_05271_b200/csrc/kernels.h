@@ -56,6 +56,7 @@ struct WpeArgs {
   int use_tc;           // 1: the Gram of this iteration came from wpe_gram_tc_kernel
   int gram_f16;         // tensor-core Gram: 1 = FP16 hi / lo split (K = 16 per MMA), 0 = TF32 split (K = 8)
   int apply_tc;         // 1: the prediction runs on the tensor cores (wpe_apply_tc_kernel)
+  int apply_f16;        // tensor-core prediction: 1 = FP16 hi / lo split (one MMA pair per tap), 0 = TF32 split (two)
   float* w_next;        // tensor-core prediction only: also write the NEXT iteration's Gram weights (psd_context 0)
 };
 /// cdbl elements of one scratch slot of the WPE solve's eigenvalue-floor fallback: A, two work matrices, B, eigenvalues

@@ -17,6 +17,8 @@
 // Block = (segment, bin), 160 threads: warp 0 issues the MMAs of a 128-frame tile; warps 1..4 stage the next
 // tile's slab rows (hi / lo split), then subtract the finished tile's prediction from the observation and
 // store it. Two staging buffers / accumulators; full / done mbarriers as in wpe_gram_tc.cu.
+#include <cuda_fp16.h>
+
 #include "kernels.h"
 
 namespace gssb {
@@ -92,7 +94,7 @@ __device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__flo
 __host__ __device__ inline int app_rows(int H) { return kTile + H; }
 // Blocks per SM the register allocation aims at. Four hide more of a tile's load -> stage -> MMA -> store latency
 // (M = 5: 3.32 -> 3.09 ms, M = 6: 3.39 -> 3.19 ms per 16-segment step); at M = 8 the serial MMA stream of the SM's one
-// tensor pipe is what binds and the fourth block only adds contention (4.39 -> 4.76 ms), so it keeps three.
+// tensor pipe is what binds and the fourth block only adds contention (4.39 -> 4.76 ms, TF32 kind), so it keeps three.
 __host__ __device__ constexpr int app_min_blocks(int M) { return M >= GSS_APPLY_3BLOCK_FROM ? 3 : 4; }
 
 }  // namespace
@@ -305,6 +307,297 @@ __global__ void __launch_bounds__(kAppThreads, app_min_blocks(M)) wpe_apply_tc_k
 }
 
 // ---------------------------------------------------------------------------
+// The same prediction on kind::f16. Every tcgen05.mma costs ~150 cycles whatever its shape or kind
+// (tools/mma_probe.cu) and this kernel is bound by its MMA stream (N = 16 / 32 per instruction), so the lever is
+// the instruction count: FP16 operands take K = 16 per MMA, i.e. one instruction per tap where TF32 needs two.
+// FP16 has a 5-bit exponent, so both operands are scaled by powers of two -- the slab by the largest magnitude of
+// the tile (128 + H frames of one bin), conj(G) by its largest entry -- and split hi + lo exactly as the TF32 kind
+// does (hi * hi + hi * lo + lo * hi, each product exact in FP32); the accumulator is rescaled exactly afterwards.
+// 11 + 11 bits hold down to 2^-14 of the tile's maximum after scaling to 2^15; the 2^-24 grid below that keeps
+// 2^-40 of the maximum absolutely, so a frame 100 dB under the loudest frame of its tile still has FP32-level
+// precision and one 140 dB under it 2^-17. The observation is kept in FP32 beside the operands: Y = obs - pred
+// subtracts from the exact value.
+// ---------------------------------------------------------------------------
+namespace {
+__device__ __forceinline__ uint32_t make_idesc_f16(int n) {  // kind::f16, FP16 x FP16 -> FP32, K-major, M = 128
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+/// 2^e that puts a magnitude bound just under 2^15, clamped so that products of two such factors stay normal floats
+__device__ __forceinline__ int scale_exp_f16(float bound) {
+  const int eb = (int)((__float_as_uint(bound) >> 23) & 255u) - 127;
+  return min(60, max(-60, 14 - eb));
+}
+__device__ __forceinline__ float pow2f(int e) { return __uint_as_float((uint32_t)(e + 127) << 23); }
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+__host__ __device__ inline size_t app_h_smem(int taps, int H) {
+  // header | B operands [tap][K core 2][hi ng0 ng1, lo ng0 ng1][8 x 16 B] | A operands [stage 2][hi, lo][K core 2][rows][16 B]
+  // | observations [stage 2][K core 4][rows][4 floats]
+  return 128 + (size_t)taps * 1024 + 4 * (size_t)(2 * app_rows(H) * 16) + 2 * (size_t)(4 * app_rows(H) * 16);
+}
+}  // namespace
+
+template <int M>
+__global__ void __launch_bounds__(kAppThreads, app_min_blocks(M)) wpe_apply_h_kernel(WpeArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const SegDev sd = a.segs[blockIdx.y];
+  if (!sd.wpe_active) return;
+  const int f = blockIdx.x;
+  const int taps = a.taps, km = taps * M, H = a.delay + taps - 1;
+  const int NROWS = app_rows(H);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);              // [2] slab of a tile is staged
+  uint64_t* done = full + 2;                                           // [2] MMAs of a tile are complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + 32);
+  float* red_a = reinterpret_cast<float*>(smem_raw + 64);              // [2 parities][4 worker warps] tile maxima
+  float* red_g = reinterpret_cast<float*>(smem_raw + 96);              // [5 warps] filter maxima
+  __half* bop = reinterpret_cast<__half*>(smem_raw + 128);
+  unsigned char* aop = smem_raw + 128 + (size_t)taps * 1024;
+  const uint32_t aop_bytes = 2u * (uint32_t)NROWS * 16u;               // one of hi / lo of one stage
+  float4* obs = reinterpret_cast<float4*>(aop + 4 * (size_t)aop_bytes);  // [stage][K core 4][NROWS]
+
+  if (tid == 0) {
+    mbar_init(&full[0], 128);
+    mbar_init(&full[1], 128);
+    mbar_init(&done[0], 1);
+    mbar_init(&done[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(128u)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // conj(G) of this bin as the B operands (real 2x2 blocks of the complex product), scaled, hi / lo split
+  int eg;
+  {
+    const float2* g = a.gconj + sd.g_wpe_off + (long long)f * km * M;
+    float mg = 0.f;
+    for (int i = tid; i < km * M; i += kAppThreads) mg = fmaxf(mg, fmaxf(fabsf(g[i].x), fabsf(g[i].y)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+    if (lane == 0) red_g[warp] = mg;
+    __syncthreads();
+    mg = fmaxf(fmaxf(fmaxf(red_g[0], red_g[1]), fmaxf(red_g[2], red_g[3])), red_g[4]);
+    eg = scale_exp_f16(mg);
+    const float sg = pow2f(eg);
+    for (int i = tid; i < taps * kKPad * kNOut; i += kAppThreads) {
+      const int u = i / (kKPad * kNOut), r = i - u * (kKPad * kNOut), kappa = r / kNOut, n = r - kappa * kNOut;
+      const int c = kappa >> 1, part = kappa & 1, c2 = n & 7, im_out = n >> 3;
+      float v = 0.f;
+      if (c < M && c2 < M) {
+        const float2 gg = g[(u * M + c) * M + c2];
+        v = (part == 0 ? (im_out ? gg.y : gg.x) : (im_out ? gg.x : -gg.y)) * sg;
+      }
+      const __half hi = __float2half_rn(v);
+      const __half lo = __float2half_rn(v - __half2float(hi));
+      // half index: (((tap, K core), n group), n row, K element); n groups 0, 1 = B_hi, 2, 3 = B_lo
+      const int at = (((u * 2 + (kappa >> 3)) * 4 + (n >> 3)) * 8 + (n & 7)) * 8 + (kappa & 7);
+      bop[at] = hi;
+      bop[at + 2 * 64] = lo;
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+  const int ntiles = (sd.T + kTile - 1) / kTile;
+
+  if (warp == 0) {
+    // ===== MMA issuer: one instruction pair per tap =====
+    if (lane == 0) {
+      const uint32_t idesc32 = make_idesc_f16(2 * kNOut), idesc16 = make_idesc_f16(kNOut);
+      const uint32_t a_lbo = (uint32_t)NROWS * 16u, a_sbo = 128u, b_lbo = 512u, b_sbo = 128u;
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i & 1;
+        mbar_wait(&full[s], (uint32_t)((i >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a_hi = smem_u32(aop) + (uint32_t)(2 * s) * aop_bytes, a_lo = a_hi + aop_bytes;
+        const uint32_t b_all = smem_u32(bop);
+        const uint32_t d = tmem_base + (uint32_t)(s * 3 * kNOut);  // [A_hi B_hi | A_hi B_lo | A_lo B_hi]
+        for (int u = 0; u < taps; ++u) {
+          const uint32_t ao = (uint32_t)u * 16u;  // rows from u
+          const uint64_t ah = make_desc(a_hi + ao, a_lbo, a_sbo), al = make_desc(a_lo + ao, a_lbo, a_sbo);
+          const uint64_t bb = make_desc(b_all + (uint32_t)u * 1024u, b_lbo, b_sbo);
+          mma_f16(d, ah, bb, idesc32, u > 0 ? 1u : 0u);               // N = 32: B_hi then B_lo
+          mma_f16(d + 2 * kNOut, al, bb, idesc16, u > 0 ? 1u : 0u);   // N = 16: B_hi
+        }
+        tc_commit(&done[s]);
+      }
+    }
+  } else {
+    // ===== workers: stage slab rows, then finish the previous tile =====
+    const int w = tid - 32;                       // 0..127
+    const int q = warp & 3;                       // tensor-memory lane quarter this warp may read
+    const float2* yf = a.yobs + sd.y_off + (long long)f * sd.T * M;
+    float2* of = a.yout + sd.y_off + (long long)f * sd.T * M;
+    float inv_s0 = 1.f, inv_s1 = 1.f;             // 2^-(ea + eg) of the tile staged in buffer 0 / 1
+
+    auto load_row = [&](int t0, int row, float (&v)[kKPad]) {
+      const int t = t0 - H + row;
+#pragma unroll
+      for (int k = 0; k < kKPad; ++k) v[k] = 0.f;
+      if (t >= 0 && t < sd.T) {
+        if constexpr (M % 2 == 0) {  // a frame is a whole number of 16-byte pieces (and 16-byte aligned): half the requests
+          const float4* p = reinterpret_cast<const float4*>(yf + (long long)t * M);
+#pragma unroll
+          for (int c = 0; c < M / 2; ++c) {
+            const float4 y = p[c];
+            v[4 * c] = y.x;
+            v[4 * c + 1] = y.y;
+            v[4 * c + 2] = y.z;
+            v[4 * c + 3] = y.w;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            const float2 y = yf[(long long)t * M + c];
+            v[2 * c] = y.x;
+            v[2 * c + 1] = y.y;
+          }
+        }
+      }
+    };
+    auto row_max = [&](const float (&v)[kKPad]) {
+      float m = 0.f;
+#pragma unroll
+      for (int k = 0; k < 2 * M; ++k) m = fmaxf(m, fabsf(v[k]));
+      return m;
+    };
+    auto stage_row = [&](int s, int row, const float (&v)[kKPad], float scl) {
+      unsigned char* hi_buf = aop + (size_t)(2 * s) * aop_bytes;
+      unsigned char* lo_buf = hi_buf + aop_bytes;
+      float4* ob = obs + (size_t)s * 4 * NROWS;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) ob[kc * NROWS + row] = make_float4(v[4 * kc], v[4 * kc + 1], v[4 * kc + 2], v[4 * kc + 3]);
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) {
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const float x0 = v[8 * kc + 2 * p] * scl, x1 = v[8 * kc + 2 * p + 1] * scl;
+          const __half2 hh = __floats2half2_rn(x0, x1);
+          const float2 hf = __half22float2(hh);
+          h[p] = h2_bits(hh);
+          l[p] = h2_bits(__floats2half2_rn(x0 - hf.x, x1 - hf.y));
+        }
+        reinterpret_cast<uint4*>(hi_buf)[kc * NROWS + row] = make_uint4(h[0], h[1], h[2], h[3]);
+        reinterpret_cast<uint4*>(lo_buf)[kc * NROWS + row] = make_uint4(l[0], l[1], l[2], l[3]);
+      }
+    };
+    auto finish_tile = [&](int i) {
+      const int s = i & 1;
+      mbar_wait(&done[s], (uint32_t)((i >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t r[kNOut], r1[kNOut], r2[kNOut];
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * 3 * kNOut);
+#define GSS_TMEM_LD16(dst, addr)                                                                                        \
+  asm volatile(                                                                                                         \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];" \
+      : "=r"(dst[0]), "=r"(dst[1]), "=r"(dst[2]), "=r"(dst[3]), "=r"(dst[4]), "=r"(dst[5]), "=r"(dst[6]), "=r"(dst[7]),  \
+        "=r"(dst[8]), "=r"(dst[9]), "=r"(dst[10]), "=r"(dst[11]), "=r"(dst[12]), "=r"(dst[13]), "=r"(dst[14]),           \
+        "=r"(dst[15])                                                                                                   \
+      : "r"(addr)                                                                                                       \
+      : "memory")
+      GSS_TMEM_LD16(r, taddr);
+      GSS_TMEM_LD16(r1, taddr + kNOut);
+      GSS_TMEM_LD16(r2, taddr + 2 * kNOut);
+#undef GSS_TMEM_LD16
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const float inv = s == 0 ? inv_s0 : inv_s1;
+#pragma unroll
+      for (int n = 0; n < kNOut; ++n)  // (hi*hi + (hi*lo + lo*hi)) rescaled: a power of two, exact
+        r[n] = __float_as_uint((__uint_as_float(r[n]) + (__uint_as_float(r1[n]) + __uint_as_float(r2[n]))) * inv);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      const int row = q * 32 + lane;            // tensor-memory lane = tile row = this thread's frame
+      const int t = i * kTile + row;
+      if (t < sd.T) {
+        const float4* ob = obs + (size_t)s * 4 * NROWS;  // the observation is slab row (row + H) of this tile
+        float o[kKPad];
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          const float4 v4 = ob[kc * NROWS + row + H];
+          o[4 * kc] = v4.x;
+          o[4 * kc + 1] = v4.y;
+          o[4 * kc + 2] = v4.z;
+          o[4 * kc + 3] = v4.w;
+        }
+        float pw = 0.f;  // squared norm of the output frame, accumulated like wpe_power_kernel does
+        float2 out[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          out[c] = make_float2(o[2 * c] - __uint_as_float(r[c]), o[2 * c + 1] - __uint_as_float(r[8 + c]));
+          pw += out[c].x * out[c].x + out[c].y * out[c].y;
+        }
+        if constexpr (M % 2 == 0) {
+          float4* p = reinterpret_cast<float4*>(of + (long long)t * M);
+#pragma unroll
+          for (int c = 0; c < M / 2; ++c) p[c] = make_float4(out[2 * c].x, out[2 * c].y, out[2 * c + 1].x, out[2 * c + 1].y);
+        } else {
+#pragma unroll
+          for (int c = 0; c < M; ++c) of[(long long)t * M + c] = out[c];
+        }
+        if (a.w_next != nullptr) {  // the next iteration's Gram weight of this frame (see wpe_apply_tc_kernel)
+          const float lambda = fmaxf((float)kPowerFloor, (float)((double)pw * (1.0 / (double)M)));
+          a.w_next[sd.w_off + (long long)f * sd.T + t] = __frcp_rn(lambda);
+        }
+      }
+    };
+
+    const bool extra = w < NROWS - kTile;  // rows past the first 128 of a tile's slab
+    float va[kKPad], vb[kKPad];
+    load_row(0, w, va);
+    if (extra) load_row(0, kTile + w, vb);
+    for (int i = 0; i < ntiles; ++i) {
+      const int s = i & 1;
+      // largest magnitude of this tile's slab: every worker's rows, exchanged across the barrier that also orders
+      // the reuse of buffer s (last read by the MMAs of tile i-2 and by the other workers' finish_tile(i-2))
+      float m = row_max(va);
+      if (extra) m = fmaxf(m, row_max(vb));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) red_a[s * 4 + q] = m;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      m = fmaxf(fmaxf(red_a[s * 4], red_a[s * 4 + 1]), fmaxf(red_a[s * 4 + 2], red_a[s * 4 + 3]));
+      const int ea = scale_exp_f16(m);
+      const float scl = pow2f(ea);
+      if (s == 0) inv_s0 = pow2f(-ea - eg);
+      else inv_s1 = pow2f(-ea - eg);
+      stage_row(s, w, va, scl);
+      if (extra) stage_row(s, kTile + w, vb, scl);
+      if (i + 1 < ntiles) {  // next tile's rows: in flight while this tile's MMAs and the epilogue run
+        load_row((i + 1) * kTile, w, va);
+        if (extra) load_row((i + 1) * kTile, kTile + w, vb);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core reads
+      mbar_arrive(&full[s]);
+      if (i > 0) finish_tile(i - 1);
+    }
+    finish_tile(ntiles - 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(128u) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
 int wpe_apply_tc_supported(int taps, int delay, int M) {
   const int H = delay + taps - 1;
   const size_t smem = 128 + sizeof(float) * (2 * (size_t)taps * 256 + 4 * (size_t)(4 * app_rows(H) * 4));
@@ -316,6 +609,13 @@ int wpe_apply_tc_supported(int taps, int delay, int M) {
 template <int M>
 static cudaError_t launch_apply_tc_m(const WpeArgs& a, int nseg, int F, cudaStream_t st) {
   const int H = a.delay + a.taps - 1;
+  if (a.apply_f16) {
+    const size_t smem = app_h_smem(a.taps, H);
+    cudaError_t e = cudaFuncSetAttribute(wpe_apply_h_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    wpe_apply_h_kernel<M><<<dim3(F, nseg), kAppThreads, smem, st>>>(a);
+    return cudaGetLastError();
+  }
   const size_t smem = 128 + sizeof(float) * (2 * (size_t)a.taps * 256 + 4 * (size_t)(4 * app_rows(H) * 4));
   cudaError_t e = cudaFuncSetAttribute(wpe_apply_tc_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
