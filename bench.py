@@ -143,8 +143,8 @@ def algorithmic_work(segs, cfg):
         T, K = ss.activity.grid.shape
         FT = F * T
         km = cfg.wpe.taps * M
-        tc_gram = g_env == "tc" or (g_env != "fp32" and M >= 3)
-        tc_apply = a_env == "tc" or (a_env != "fp32" and M >= 5)
+        tc_gram = g_env == "tc" or (g_env != "fp32" and M >= 2)
+        tc_apply = a_env == "tc" or (a_env != "fp32" and M >= 4)
         w["stft"]["bytes"] += 4 * M * N + 8 * FT * M
         w["stft"]["flops"] += M * T * (2.5 * n * math.log2(n) + n)
         if J:
@@ -157,15 +157,16 @@ def algorithmic_work(segs, cfg):
             w["wpe_apply"]["flops"] += J * FT * 8 * km * M
             w["wpe_apply"]["bytes"] += J * 2 * 8 * FT * M
         if J and tc_gram:
-            # tensor-core Gram: executed TF32 flops (3xTF32 split; a 128 x NR accumulator plus the corner block as
-            # an M = 64 MMA of N2 columns; the tensor core's cost floor is that of M = 128 for either)
+            # tensor-core Gram: executed tensor flops (hi/lo split: 3 MMAs per product; a 128 x NR accumulator plus,
+            # where an Im a row lies beyond row 127, the corner block as an M = 64 MMA of N2 columns)
             kmp = (km + 7) // 8 * 8
             nr = (2 * kmp + 16 + 15) // 16 * 16
-            n2 = max(0, nr - 128)
+            nr = (nr + 31) // 32 * 32 if nr < 128 else nr  # kernels.h wpe_tc_operand_rows
+            n2 = max(0, nr - 128) if kmp + km > 128 else 0
             w["wpe_gram"]["tensor_flops"] = (w["wpe_gram"].get("tensor_flops", 0.0) +
                                              J * FT * 3 * 2 * (128 * nr + 64 * n2))
         if J and tc_apply:
-            # tensor-core prediction: per frame and tap 2 k-steps of 8, A_hi x [B_hi | B_lo] (N = 32) + A_lo x B_hi (N = 16)
+            # tensor-core prediction: per frame and tap K = 16, A_hi x [B_hi | B_lo] (N = 32) + A_lo x B_hi (N = 16)
             w["wpe_apply"]["tensor_flops"] = w["wpe_apply"].get("tensor_flops", 0.0) + J * FT * cfg.wpe.taps * 2 * 2 * 8 * 48
         w["em_pass"]["flops"] += (I + 1) * FT * (3 * M * M + 4 * M * M * K + 20 * K)
         w["em_pass"]["bytes"] += (I + 1) * (8 * FT * M + T * K)
@@ -188,7 +189,13 @@ def sum_work(calls):
     return total
 
 
-def kernel_table(kms, steps, work, nseg, hbm_peak, tf32_peak, fp32_peak, peak_src, traffic):
+def tensor_peak(kernel, bf16_peak):
+    """(dense peak of the MMA kind the kernel runs, its name): kind::f16 at the 16-bit rate, kind::tf32 at half of it."""
+    env = {"wpe_gram": "GSS_B200_WPE_GRAM_KIND", "wpe_apply": "GSS_B200_WPE_APPLY_KIND"}[kernel]
+    return (0.5 * bf16_peak, "TF32 dense = 0.5 x bf16 ") if os.environ.get(env) == "tf32" else (bf16_peak, "FP16 dense = bf16 ")
+
+
+def kernel_table(kms, steps, work, nseg, hbm_peak, bf16_peak, fp32_peak, peak_src, traffic):
     """Per kernel class: ms per step, launches, the roofline that bounds it and the fraction reached."""
     tc_gram = tc_apply = True  # a class is tensor-bound when any of its segments ran the tcgen05 kernel (tensor_flops > 0)
     kernels = {}
@@ -205,16 +212,17 @@ def kernel_table(kms, steps, work, nseg, hbm_peak, tf32_peak, fp32_peak, peak_sr
         kernels[name] = {"ms_per_step": round(per_step, 4), "launches_per_step": n // steps, "bound": bound,
                          "achieved": round(ach, 2), "peak": round(peak, 2),
                          "unit": "TFLOP/s" if bound == "fp32" else "GB/s", "frac": round(ach / peak, 4)}
-        for kname, on, note in (("wpe_gram", tc_gram, ""), ("wpe_apply", tc_apply,
-                                "; N = 16-32 MMAs re-stream their 128 x 8 A tile from shared memory, which is what "
-                                "bounds them")):
+        note = ("; a tcgen05.mma costs ~150 cycles whatever its M, N and kind (tools/mma_probe.cu), so a kernel of "
+                "small-N MMAs is bound by its instruction count, not by the dense peak")
+        for kname, on in (("wpe_gram", tc_gram), ("wpe_apply", tc_apply)):
             if name == kname and on and work[name].get("tensor_flops"):
-                # tcgen05 kind::tf32: `achieved` stays the ALGORITHMIC (FP32-equivalent) rate; the executed tensor
-                # rate (3 MMAs per product, padded tiles) is reported beside it
+                # tcgen05: `achieved` stays the ALGORITHMIC (FP32-equivalent) rate; the executed tensor rate (3 MMAs
+                # per product, padded tiles) is reported beside it
+                tpeak, tname = tensor_peak(name, bf16_peak)
                 ex = work[name]["tensor_flops"] / (per_step * 1e-3) * 1e-12
-                kernels[name].update({"bound": "tensor", "peak": round(tf32_peak, 2), "frac": round(ach / tf32_peak, 4),
-                                      "executed_tensor_tflops": round(ex, 1), "executed_frac": round(ex / tf32_peak, 4),
-                                      "peak_note": "TF32 dense = 0.5 x bf16 " + peak_src + note})
+                kernels[name].update({"bound": "tensor", "peak": round(tpeak, 2), "frac": round(ach / tpeak, 4),
+                                      "executed_tensor_tflops": round(ex, 1), "executed_frac": round(ex / tpeak, 4),
+                                      "peak_note": tname + peak_src + note})
         if name in traffic and nseg:
             kernels[name]["traffic_bytes_per_launch"] = int(traffic[name]["dram_bytes_per_segment_launch"] * nseg)
     return kernels
@@ -235,7 +243,7 @@ class Bench:
         self.ctx = gss.default_context(local_rank)
         self.stream = torch.cuda.ExternalStream(self.ctx.stream, device=torch.device("cuda", local_rank))
         self.hbm_peak, bf16_peak, self.peak_src = _peaks()
-        self.tf32_peak = 0.5 * bf16_peak
+        self.bf16_peak = bf16_peak
         self.fp32_peak = self.ctx.fp32_peak_tflops()
         self.traffic = _ncu_traffic()
 
@@ -361,7 +369,7 @@ def side_config(b, name, calls, steps, warmup, scaling, label, extra=None):
         return None
     work = sum_work(calls)
     nseg = sum(len(segs) for _, segs in calls)
-    kernels = kernel_table(r["kms"], steps, work, nseg, b.hbm_peak, b.tf32_peak, b.fp32_peak, b.peak_src, {})
+    kernels = kernel_table(r["kms"], steps, work, nseg, b.hbm_peak, b.bf16_peak, b.fp32_peak, b.peak_src, {})
     top = top_kernel(kernels)
     res.update({"workload": label, "steps": steps,
                 "kernels_ms_per_step": {k: v["ms_per_step"] for k, v in kernels.items()},
@@ -408,7 +416,7 @@ def run_ours(args, rank, world, local_rank):
     line = None
     if rank == 0:
         work = sum_work(calls)
-        kernels = kernel_table(r["kms"], args.steps, work, nseg, b.hbm_peak, b.tf32_peak, b.fp32_peak, b.peak_src,
+        kernels = kernel_table(r["kms"], args.steps, work, nseg, b.hbm_peak, b.bf16_peak, b.fp32_peak, b.peak_src,
                                b.traffic)
         top = top_kernel(kernels)
         roof = None

@@ -74,9 +74,10 @@ struct gss_b200_ctx {
   double kernel_ms[GSS_B200_NUM_KERNELS] = {0};
   long long kernel_launches[GSS_B200_NUM_KERNELS] = {0};
   // WPE kernel choice: 2 = by shape (default), 1 = tcgen05 wherever it is supported (GSS_B200_WPE_GRAM / _APPLY = tc),
-  // 0 = the FP32-FMA kernels (= fp32). By shape: the 128-row MMA tiles pay off from 3 channels (Gram) / 5 channels
-  // (prediction) upwards; below that the FP32 kernels win (tools/shape_bench.py: prediction 0.78 vs 3.18 ms at M = 2,
-  // 1.98 vs 3.21 at M = 4, 3.02 vs 3.32 at M = 5; Gram 6.85 vs 8.46 ms at M = 2, 16.9 vs 9.4 at M = 4).
+  // 0 = the FP32-FMA kernels (= fp32). By shape, with the FP16 kinds (tools/shape_bench.py, 16 segments, ms per step):
+  // the Gram pays off from 2 channels (5.56 + 0.73 more in the solve, which reads the wider cell, against 6.85 at
+  // M = 2; 3.57 FP32 at M = 1), the prediction from 4 (1.59 and the fused power pass against 1.98 + 0.33 at M = 4; a
+  // tie at M = 3; 1.54 against 0.78 at M = 2).
   int wpe_gram_tc = 2;
   int wpe_gram_f16 = 1;      // tensor-core Gram operand split: 1 = FP16 (K = 16 per MMA), 0 = TF32 (GSS_B200_WPE_GRAM_KIND = tf32)
   int wpe_apply_tc = 2;
@@ -516,7 +517,7 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
   }
   if (need.wpe) {
     g.w = m.get<float>(o_w);
-    g.use_tc = (c->wpe_gram_tc == 1 || (c->wpe_gram_tc == 2 && M >= 3)) && wpe_tc_supported(km, M) && g.max_wchunks == 1;
+    g.use_tc = (c->wpe_gram_tc == 1 || (c->wpe_gram_tc == 2 && M >= 2)) && wpe_tc_supported(km, M) && g.max_wchunks == 1;
     if (g.use_tc)
       g.gram_raw = m.get<float>((size_t)o_f * wpe_tc_cell_floats(km, M));
     else
@@ -569,7 +570,7 @@ gss_status run_wpe(gss_b200_ctx* c, Group& g, const gss_wpe_config& w, int first
   a.use_tc = g.use_tc;
   a.gram_f16 = c->wpe_gram_f16;
   a.apply_f16 = c->wpe_apply_f16;
-  a.apply_tc = (c->wpe_apply_tc == 1 || (c->wpe_apply_tc == 2 && g.M >= 5)) &&
+  a.apply_tc = (c->wpe_apply_tc == 1 || (c->wpe_apply_tc == 2 && g.M >= 4)) &&
                wpe_apply_tc_supported(w.taps, w.delay, g.M);
   a.debug_rp = nullptr;
   a.w_next = nullptr;

@@ -64,6 +64,13 @@ __host__ __device__ inline int wpe_fallback_slot_elems(int km, int M) { return 3
 /// cfloat elements of one (segment, bin, chunk) Gram cell
 int wpe_gram_cell_elems(int km, int M);
 /// tensor-core Gram (wpe_gram_tc.cu)
+/// Rows of the staged operand = columns of the accumulator D1: [Re a | Im a] (each padded to 8) + 16 current-frame rows,
+/// rounded up to 16; up to one 128-row tile it is rounded to 32 so that a quarter of the columns is a whole number of
+/// 8-column tensor-memory loads (M = 1, 3 at 10 taps).
+__host__ __device__ inline int wpe_tc_operand_rows(int km) {
+  const int kmp = (km + 7) & ~7, nr = ((2 * kmp + 16 + 15) / 16) * 16;
+  return nr < 128 ? (nr + 31) & ~31 : nr;
+}
 int wpe_tc_supported(int km, int M);
 int wpe_tc_cell_floats(int km, int M);
 int wpe_tc_rows(int km, int M);

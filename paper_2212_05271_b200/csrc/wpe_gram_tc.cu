@@ -43,7 +43,7 @@ constexpr int kAccPerThread = 56;           // register accumulators per thread:
 // Row layout of the staged operand S (each block padded to a multiple of 8 rows so that a row group is
 // homogeneous): [Re a (KMP)] [Im a (KMP)] [Re y (8)] [Im y (8)] [zero pad to a multiple of 16].
 __host__ __device__ inline int tc_kmp(int km) { return (km + 7) & ~7; }
-__host__ __device__ inline int tc_rows(int km, int M) { return ((2 * tc_kmp(km) + 16 + 15) / 16) * 16; }  // NR
+__host__ __device__ inline int tc_rows(int km, int M) { return wpe_tc_operand_rows(km); }  // NR
 __host__ __device__ inline int tc_buf_rows(int km, int M) { return tc_rows(km, M) < 128 ? 128 : tc_rows(km, M); }
 __host__ __device__ inline int tc_n2(int km, int M) { return tc_rows(km, M) > 128 ? tc_rows(km, M) - 128 : 0; }
 __host__ __device__ inline int tc_cols(int km, int M) { return tc_rows(km, M) + tc_n2(km, M); }         // D1 | D2

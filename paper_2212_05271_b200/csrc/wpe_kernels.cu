@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kSolveThreads, 4) wpe_solve2_kernel(WpeArgs a)
   const int lane = tid & 31, warp = tid >> 5;
   const float2* tiles = a.gram + (sd.wcell_off + (long long)f * sd.wchunks) * ntiles * kTileElems;
   const long long chunk_stride = (long long)ntiles * kTileElems;
-  const int KMP = (km + 7) & ~7, NR = ((2 * KMP + 16 + 15) / 16) * 16, N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
+  const int KMP = (km + 7) & ~7, NR = wpe_tc_operand_rows(km), N2 = NR > 128 ? NR - 128 : 0, NCT = NR + N2;
   const float* raw = a.gram_raw + (sd.wcell_off + (long long)f) * (long long)(128 * NCT);
 
   // hermitized R[i][j] (j <= i) and P[i][c] in double from this iteration's Gram (either producer)
