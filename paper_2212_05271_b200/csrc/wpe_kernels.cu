@@ -268,7 +268,12 @@ __global__ void __launch_bounds__(kGramThreads, 1) wpe_gram_kernel(WpeArgs a) {
 // A pivot <= 0 fails like Eigen's LLT and takes the eigenvalue-floor fallback (numerics.hpp:58-73, 90-93).
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int kSolveThreads = 128;
+#ifndef GSS_SOLVE_THREADS
+#define GSS_SOLVE_THREADS 128
+#define GSS_SOLVE_MINB 4
+#endif
+constexpr int kSolveThreads = GSS_SOLVE_THREADS;
+constexpr int kSolveTY = kSolveThreads / 16;  // thread rows of the trailing update's 16-column thread grid
 constexpr int kPB = 8;
 __device__ __forceinline__ int tri(int i) { return i * (i + 1) / 2; }
 }  // namespace
@@ -409,7 +414,7 @@ __device__ bool block_eig_floor_solve(cdbl* A, int n, cdbl* B, int nrhs, cdbl* V
   return true;
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 4) wpe_solve2_kernel(WpeArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, GSS_SOLVE_MINB) wpe_solve2_kernel(WpeArgs a) {
   extern __shared__ float4 smem_f4[];
   const SegDev sd = a.segs[blockIdx.y];
   if (!sd.wpe_active) return;
@@ -582,8 +587,8 @@ __global__ void __launch_bounds__(kSolveThreads, 4) wpe_solve2_kernel(WpeArgs a)
     {
       const int ty = tid >> 4, tx = tid & 15;
       const int nrows = nbelow + M;
-      for (int t = ty; t < nrows; t += 16) {
-        const int t1 = t + 8;
+      for (int t = ty; t < nrows; t += 2 * kSolveTY) {
+        const int t1 = t + kSolveTY;
         const bool has1 = t1 < nrows;
         const bool isw0 = t >= nbelow, isw1 = has1 && t1 >= nbelow;
         cdbl* row0 = isw0 ? W + (t - nbelow) * km : Lp + tri(r0 + t);
