@@ -143,7 +143,7 @@ def algorithmic_work(segs, cfg):
         T, K = ss.activity.grid.shape
         FT = F * T
         km = cfg.wpe.taps * M
-        tc_gram = g_env == "tc" or (g_env != "fp32" and M >= 2)
+        tc_gram = g_env == "tc" or (g_env != "fp32" and M >= 4)
         tc_apply = a_env == "tc" or (a_env != "fp32" and M >= 4)
         w["stft"]["bytes"] += 4 * M * N + 8 * FT * M
         w["stft"]["flops"] += M * T * (2.5 * n * math.log2(n) + n)

@@ -75,9 +75,11 @@ struct gss_b200_ctx {
   long long kernel_launches[GSS_B200_NUM_KERNELS] = {0};
   // WPE kernel choice: 2 = by shape (default), 1 = tcgen05 wherever it is supported (GSS_B200_WPE_GRAM / _APPLY = tc),
   // 0 = the FP32-FMA kernels (= fp32). By shape, with the FP16 kinds (tools/shape_bench.py, 16 segments, ms per step):
-  // the Gram pays off from 2 channels (5.56 + 0.73 more in the solve, which reads the wider cell, against 6.85 at
-  // M = 2; 3.57 FP32 at M = 1), the prediction from 4 (1.59 and the fused power pass against 1.98 + 0.33 at M = 4; a
-  // tie at M = 3; 1.54 against 0.78 at M = 2).
+  // both from 4 channels. Gram: 6.6 against 16.9 at M = 4. At M = 2, 3 the tensor kernel is faster too (5.56 against
+  // 6.85, 6.62 against 9.95) but the split's 1e-6 Gram error -- against 1e-7 of an FP32 sum -- tips a few barely
+  // positive-definite bins of those more-sources-than-channels shapes into the solve's eigenvalue-floor fallback in the
+  // third iteration (2.0 instead of 0.28 ms for that launch), so they keep the FP32 kernel. Prediction: 1.59 and the
+  // fused power pass against 1.98 + 0.33 at M = 4; a tie at M = 3; 1.54 against 0.78 at M = 2.
   int wpe_gram_tc = 2;
   int wpe_gram_f16 = 1;      // tensor-core Gram operand split: 1 = FP16 (K = 16 per MMA), 0 = TF32 (GSS_B200_WPE_GRAM_KIND = tf32)
   int wpe_apply_tc = 2;
@@ -517,7 +519,7 @@ gss_status build_group(gss_b200_ctx* c, Group& g, int M, int K_for_tier, int F, 
   }
   if (need.wpe) {
     g.w = m.get<float>(o_w);
-    g.use_tc = (c->wpe_gram_tc == 1 || (c->wpe_gram_tc == 2 && M >= 2)) && wpe_tc_supported(km, M) && g.max_wchunks == 1;
+    g.use_tc = (c->wpe_gram_tc == 1 || (c->wpe_gram_tc == 2 && M >= 4)) && wpe_tc_supported(km, M) && g.max_wchunks == 1;
     if (g.use_tc)
       g.gram_raw = m.get<float>((size_t)o_f * wpe_tc_cell_floats(km, M));
     else
