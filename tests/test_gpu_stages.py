@@ -200,6 +200,60 @@ def test_wpe_tensor_core_kernels_match_the_fp32_kernels_at_full_width(gss):
     assert np.abs(got - want).max() < 1e-3 * np.abs(want).max()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [8, 5])
+def test_wpe_tensor_core_prediction_over_a_wide_dynamic_range(gss, m):
+    # The FP16-kind prediction scales a 140-frame tile by one power of two. Quiet frames far below the loudest frame of
+    # their tile keep fewer bits (FP32-level down to -100 dB, 2^-17 at -140 dB), so the check is
+    # per frame, relative to that frame: the tensor-core kernels against the FP32-FMA kernels on the same input.
+    import os
+    rng = np.random.RandomState(40 + m)
+    f, t = 5, 900
+    s = (rng.randn(f, t, m) + 1j * rng.randn(f, t, m)).astype(np.complex64)
+    y = s.copy()
+    y[:, 3:, :] += 0.5 * s[:, :-3, :]
+    env = np.ones(t, np.float32)
+    env[100:130] = 1e3      # a burst ...
+    env[130:400] = 1e-4     # ... followed by 140 dB less, first inside the burst's tile, then in tiles of its own
+    env[500:540] = 0.0      # digital silence
+    env[600:] *= np.exp(2 * rng.randn(t - 600)).astype(np.float32)
+    y *= env[None, :, None]
+    y[0] *= 1e-5
+    y[4] *= 1e4
+    cfg = gss.wpe.WpeConfig(10, 2, 1, 0, 1e-10)  # one iteration, FP32 Gram in both runs: the filters are the same bits
+    old = {k: os.environ.get(k) for k in ("GSS_B200_WPE_APPLY", "GSS_B200_WPE_GRAM")}
+    res = {}
+    try:
+        for kind in ("tc", "fp32"):
+            os.environ["GSS_B200_WPE_GRAM"] = "fp32"
+            os.environ["GSS_B200_WPE_APPLY"] = kind
+            ctx = gss.Context(0)  # the switches are read when a context is created
+            res[kind] = gss.wpe.dereverberate(spec(gss, y), cfg, ctx).data
+            ctx.close()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    got, want = res["tc"], res["fp32"]
+    assert np.isfinite(got).all()
+    # Y_t = obs_t - sum over the window: where a quiet frame follows a burst the difference cancels, and any FP32
+    # evaluation is only good relative to the window's largest frame. That is the scale an error is measured on.
+    h = cfg.delay + cfg.taps - 1
+    fn = np.sqrt((np.abs(y) ** 2).sum(2))                       # (f, t) frame norms of the input
+    pad = np.concatenate([np.zeros((f, h), fn.dtype), fn], 1)
+    scale = np.max(np.stack([pad[:, u: u + t] for u in range(h + 1)]), 0)  # largest of frames t-h .. t
+    num = np.sqrt((np.abs(got - want) ** 2).sum(2))
+    live = scale > 0
+    assert np.array_equal(got[~live], want[~live])              # silent stretches stay exactly silent
+    worst = (num[live] / scale[live]).max()
+    print(f"[prediction dynamic range M={m}] worst per-frame difference relative to its window {worst:.2e}, "
+          f"overall {rel_fro(got, want):.2e}")
+    assert worst < 2e-5, worst  # measured 2.2e-6 (M = 8), 9.6e-7 (M = 5)
+    assert rel_fro(got, want) < 1e-5
+
+
 def _gram_float64(y, taps, delay, floor=1e-10):
     """R = sum_t w_t a_t a_t^H and P = sum_t w_t a_t y_t^H in float64, weights as the device forms them (wpe.hpp:40-89)."""
     f, t, m = y.shape
