@@ -212,8 +212,8 @@ def kernel_table(kms, steps, work, nseg, hbm_peak, bf16_peak, fp32_peak, peak_sr
         kernels[name] = {"ms_per_step": round(per_step, 4), "launches_per_step": n // steps, "bound": bound,
                          "achieved": round(ach, 2), "peak": round(peak, 2),
                          "unit": "TFLOP/s" if bound == "fp32" else "GB/s", "frac": round(ach / peak, 4)}
-        note = ("; a tcgen05.mma costs ~150 cycles whatever its M, N and kind (tools/mma_probe.cu), so a kernel of "
-                "small-N MMAs is bound by its instruction count, not by the dense peak")
+        note = ("; a thread issues one tcgen05.mma per ~100 - 150 cycles whatever its M, N and kind (tools/mma_probe.cu), "
+                "so a kernel of small-N MMAs pays for its instruction count and stays far from the dense peak")
         for kname, on in (("wpe_gram", tc_gram), ("wpe_apply", tc_apply)):
             if name == kname and on and work[name].get("tensor_flops"):
                 # tcgen05: `achieved` stays the ALGORITHMIC (FP32-equivalent) rate; the executed tensor rate (3 MMAs

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <utility>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -48,7 +49,8 @@ __device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // accs = number of distinct accumulators the chain rotates over (1 = every MMA depends on the previous one's D)
-__global__ void __launch_bounds__(128, 1) probe(long long* out, int m, int n, int chain, int accs, int reps, int f16) {
+// tmem_cols: 512 with one CTA per SM, 256 with two (both then issue into the SM's one tensor pipe)
+__global__ void __launch_bounds__(128, 2) probe(long long* out, int m, int n, int chain, int accs, int reps, int f16, uint32_t tmem_cols) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
@@ -59,7 +61,7 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int m, int n, in
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512u) : "memory");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(tmem_cols) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int m, int n, in
   __syncthreads();
   if (tid < 32) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512u) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(tmem_cols) : "memory");
   }
 }
 
@@ -109,7 +111,7 @@ int main() {
       long long c[2] = {0, 0};
       int k = 0;
       for (int chain : {32, 64}) {
-        probe<<<148, 128, 48 * 1024>>>(d, s[0], s[1], chain, accs, 20, f16);
+        probe<<<148, 128, 48 * 1024>>>(d, s[0], s[1], chain, accs, 20, f16, 512u);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
           printf("M=%d N=%d: %s\n", s[0], s[1], cudaGetErrorString(e));
@@ -121,6 +123,18 @@ int main() {
       printf("%s M=%3d N=%3d accumulators=%d: %7.1f cycles/MMA  (%.0f MAC/clk; chain32 %lld, chain64 %lld)\n", f16 ? "f16 K=16 " : "tf32 K=8 ", s[0], s[1], accs, per,
              (double)s[0] * s[1] * (f16 ? 16 : 8) / per, c[0], c[1]);
     }
+  }
+  // two CTAs per SM, each with its own issuing thread: is the 150 cycles a per-thread issue cost or the pipe's?
+  for (auto& s : {std::pair<int, int>{128, 32}, {128, 176}, {64, 48}}) {
+    long long c[2] = {0, 0};
+    int k = 0;
+    for (int chain : {32, 64}) {
+      probe<<<296, 128, 48 * 1024>>>(d, s.first, s.second, chain, 1, 20, 0, 256u);
+      if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+      cudaMemcpy(&c[k++], d, 8, cudaMemcpyDeviceToHost);
+    }
+    printf("tf32 K=8  M=%3d N=%3d, TWO CTAs per SM issuing at once: %7.1f cycles/MMA per CTA\n", s.first, s.second,
+           (double)(c[1] - c[0]) / 32.0);
   }
   return 0;
 }
