@@ -274,7 +274,7 @@ def _gram_float64(y, taps, delay, floor=1e-10):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("kind", ["f16", "tf32"])
-@pytest.mark.parametrize("m, t", [(8, 700), (4, 333), (5, 1000)])
+@pytest.mark.parametrize("m, t", [(8, 700), (4, 333), (5, 1000), (1, 300), (2, 350), (3, 400), (6, 500), (7, 450)])
 def test_wpe_tensor_core_gram_over_a_wide_dynamic_range(gss, kind, m, t):
     # The FP16 kind scales every 128-frame stage by a power of two; loud bursts next to near-silence, exact zeros
     # and very small / very large overall levels are where a fixed-range format would lose the Gram. Both kinds must
